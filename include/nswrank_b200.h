@@ -1,0 +1,183 @@
+/*
+ * nswrank_b200 -- B200-native drop-in for the NSW fair-ranking ascent path.
+ *
+ * C ABI of libnswrank_b200.so: plain pointers and sizes, no torch types.
+ * Every entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/nswrank, version 0.1.0).  The reference is pure
+ * Python/numpy, so the binding a maintainer would add on the reference side
+ * is a ctypes stub; it is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Host pointers are float64 row-major arrays in the reference's layouts:
+ *     relevance [U][n], exposure [m-1], policy [U][n][m].
+ *   - Device pointers (the *_dev / operator entry points) are stream-ordered;
+ *     `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Every function returns an nsw_status; nsw_last_error() gives the text.
+ *     The Python host layer maps the codes onto the reference's exception
+ *     classes (reference core.py:20-33): SHAPE -> ShapeError,
+ *     DOMAIN -> DomainError, SOLVER -> SolverError, STATE -> StateError.
+ */
+#ifndef NSWRANK_B200_H
+#define NSWRANK_B200_H
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NSW_OK = 0,
+  NSW_ERR_SHAPE = 1,        /* ShapeError   (reference core.py:20)          */
+  NSW_ERR_DOMAIN = 2,       /* DomainError  (reference core.py:24)          */
+  NSW_ERR_STATE = 3,        /* StateError   (reference core.py:28)          */
+  NSW_ERR_SOLVER = 4,       /* SolverError  (reference core.py:32)          */
+  NSW_ERR_UNSUPPORTED = 5,  /* shape/dtype has no compiled kernel variant   */
+  NSW_ERR_CUDA = 6,         /* CUDA runtime failure                         */
+  NSW_ERR_ARG = 7           /* bad argument (null pointer, bad enum)        */
+} nsw_status;
+
+typedef enum { NSW_F32 = 0, NSW_F64 = 1 } nsw_dtype;
+
+typedef enum {
+  NSW_SCHEDULE_FIXED = 0,     /* exactly sinkhorn_max_iters inner iterations per solve */
+  NSW_SCHEDULE_TOLERANCE = 1  /* reference default: lock-step stop at residual <= tol  */
+} nsw_schedule;
+
+/* Mirrors SolverConfig (reference core.py:171-201) field for field. */
+typedef struct {
+  double epsilon;
+  int32_t sinkhorn_max_iters;
+  double sinkhorn_tol;
+  int32_t outer_max_iters;
+  double grad_threshold;
+  double adam_lr;
+  double adam_beta1;
+  double adam_beta2;
+  double adam_eps;
+  int32_t warm_start;
+} nsw_solver_config;
+
+/* Device-side options (not part of the reference config). */
+typedef struct {
+  int32_t dtype;          /* nsw_dtype: F32 throughput path, F64 parity path        */
+  int32_t schedule;       /* nsw_schedule                                           */
+  int32_t device;         /* CUDA device ordinal                                    */
+  int32_t variant;        /* -1 = automatic tile choice, else index into the table  */
+  int32_t use_graph;      /* capture the outer step in a CUDA graph (1) or not (0)  */
+  int32_t check_every;    /* host polls the stop flag every N outer steps           */
+} nsw_device_options;
+
+/* Returned trace; mirrors SolveTrace (reference solver.py:125-135). */
+typedef struct {
+  int32_t steps;            /* number of recorded outer iterations               */
+  double* objective;        /* caller-allocated [outer_max_iters]                */
+  double* grad_norm;        /* caller-allocated [outer_max_iters]                */
+  int32_t* sinkhorn_iterations;  /* caller-allocated [outer_max_iters]           */
+  double* wall_time;        /* caller-allocated [outer_max_iters], seconds/step  */
+} nsw_trace;
+
+const char* nsw_last_error(void);
+const char* nsw_version(void);
+
+/* ------------------------------------------------------------------------ *
+ * 1. Whole solve, host buffers.                                           *
+ *    Replaces solve_fair_ranking (reference solver.py:138-241).  The best  *
+ *    iterate's policy (solver.py:217-219, 241) is written to policy_out    *
+ *    [U][n][m] float64; the trace to *trace.                               *
+ * ------------------------------------------------------------------------ */
+nsw_status nsw_solve_fair_ranking(const double* relevance, const double* exposure,
+                                  int32_t num_users, int32_t num_items, int32_t num_positions,
+                                  const nsw_solver_config* config, const nsw_device_options* options,
+                                  double* policy_out, nsw_trace* trace);
+
+/* ------------------------------------------------------------------------ *
+ * 2. Step-level solver handle: the same solve split into stream-ordered    *
+ *    pieces so a caller can shard users over GPUs and run the per-step     *
+ *    impact exchange (reference solver.py:206) itself.                     *
+ * ------------------------------------------------------------------------ */
+typedef struct nsw_solver nsw_solver;
+
+/* users_local: this rank's contiguous user block; relevance_local [users_local][n]
+ * float64 host; rel_sq_sum [n] = sum over ALL users of r_ui^2 (closed-form
+ * gradient norm, solver.py:211); world = number of impact partials the
+ * finalize step sums (1 for a single GPU). */
+nsw_status nsw_solver_create(const double* relevance_local, const double* exposure,
+                             int32_t users_local, int32_t num_items, int32_t num_positions,
+                             const double* rel_sq_sum, int32_t world,
+                             const nsw_solver_config* config, const nsw_device_options* options,
+                             nsw_solver** out);
+nsw_status nsw_solver_destroy(nsw_solver* s);
+
+/* Device pointers of the impact exchange: local [n] float64 (written by
+ * nsw_solver_local_step), gathered [world][n] float64 (read by
+ * nsw_solver_finalize).  May be rebound to caller-owned device buffers. */
+nsw_status nsw_solver_exchange_buffers(nsw_solver* s, void** local_dev, void** gathered_dev);
+nsw_status nsw_solver_bind_exchange(nsw_solver* s, void* local_dev, void* gathered_dev);
+
+/* One outer step minus the exchange: [backward of step k-1 + Adam +]
+ * forward of step k + local impact reduction.  No-op once finished. */
+nsw_status nsw_solver_local_step(nsw_solver* s, void* stream);
+/* Objective, gradient norm, best-iterate and stop decisions from the
+ * gathered impacts (solver.py:206-223).  No-op once finished. */
+nsw_status nsw_solver_finalize(nsw_solver* s, void* stream);
+/* local_step + finalize, world must be 1; uses the solver's own stream and
+ * CUDA graph.  Runs at most max_steps outer steps; *done = 1 when finished. */
+nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done);
+/* Host view of the device state: phase (0 init, 1 running, 2 stop pending,
+ * 3 finished), recorded steps, error bits. */
+nsw_status nsw_solver_status(nsw_solver* s, int32_t* phase, int32_t* steps, int32_t* errors);
+nsw_status nsw_solver_stream(nsw_solver* s, void** stream);
+/* Best policy [users_local][n][m] float64 and the trace (host). */
+nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace);
+
+/* Raw state access for tests and one-step parity (host float64 buffers):
+ * field = "cost" | "adam_m" | "adam_v" [U][n][m], "alpha" [U][n], "beta" [U][m],
+ * "hist" [U][T+1][m], "partial" [U][n], "imp" [n], "xbest" [U][n][m].
+ * nsw_solver_set_state also takes "adam_step" / "phase" through `scalar`. */
+nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t count);
+nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, size_t count);
+nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value);
+/* Number of kernel launches issued by the solver so far (evidence counter). */
+int64_t nsw_solver_launch_count(nsw_solver* s);
+/* Kernel variant chosen for the fused step: M, rows/thread, threads/CTA. */
+nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT, int32_t* smem_bytes);
+/* Device time (ms) of the last N fused step kernels, CUDA events. */
+nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
+                                 float* ms_fused_kernel);
+
+/* ------------------------------------------------------------------------ *
+ * 3. Inner operator seam (device pointers, fixed schedule).                *
+ *    nsw_sinkhorn_batch_*  replaces _sinkhorn_batch(..., tol<=0, record)   *
+ *        (reference sinkhorn.py:204-255): log_kernel [B][n][m],            *
+ *        log_v_init [B][m] -> plan [B][n][m], log_u [B][n], log_v [B][m],  *
+ *        log_v_hist [T][B][m].                                             *
+ *    nsw_sinkhorn_backward_batch_* replaces _sinkhorn_backward_batch       *
+ *        (reference sinkhorn.py:258-309) -> grad_log_kernel [B][n][m].     *
+ *    Marginals are the ranking marginals (sinkhorn.py:55-60).              *
+ * ------------------------------------------------------------------------ */
+nsw_status nsw_sinkhorn_batch_f64(const double* log_kernel, const double* log_v_init, int32_t B,
+                                  int32_t n, int32_t m, int32_t iters, double* plan, double* log_u,
+                                  double* log_v, double* log_v_hist, void* stream);
+nsw_status nsw_sinkhorn_batch_f32(const float* log_kernel, const float* log_v_init, int32_t B,
+                                  int32_t n, int32_t m, int32_t iters, float* plan, float* log_u,
+                                  float* log_v, float* log_v_hist, void* stream);
+nsw_status nsw_sinkhorn_backward_batch_f64(const double* log_kernel, const double* log_v_hist,
+                                           const double* log_v_init, const double* grad_plan,
+                                           const double* plan, const double* log_u_final, int32_t B,
+                                           int32_t n, int32_t m, int32_t iters,
+                                           double* grad_log_kernel, void* stream);
+nsw_status nsw_sinkhorn_backward_batch_f32(const float* log_kernel, const float* log_v_hist,
+                                           const float* log_v_init, const float* grad_plan,
+                                           const float* plan, const float* log_u_final, int32_t B,
+                                           int32_t n, int32_t m, int32_t iters,
+                                           float* grad_log_kernel, void* stream);
+
+/* Whether a (dtype, n, m, iters) problem has a compiled tile variant. */
+int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NSWRANK_B200_H */

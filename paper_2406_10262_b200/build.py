@@ -1,0 +1,108 @@
+"""Build libnswrank_b200.so in-tree (nvcc, sm_100a).
+
+    python -m paper_2406_10262_b200.build [-j N] [--force]
+
+Each (scalar type, M) instantiation of the fused step kernel is its own
+translation unit so they compile in parallel.  Objects go to
+``paper_2406_10262_b200/build/``; the shared library lands next to this file
+(git-ignored, but it travels to the GPU box with the gpurun snapshot).
+"""
+
+from __future__ import annotations
+
+import argparse
+import concurrent.futures as cf
+import os
+import shutil
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+BUILD = os.path.join(HERE, "build")
+REPO = os.path.dirname(HERE)
+LIB = os.path.join(HERE, "libnswrank_b200.so")
+INCLUDE = os.path.join(REPO, "include")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", CSRC]
+
+# (f64?, M) instantiations of the fused step kernel; any m <= 32 pads up.
+INSTANCES = [(f64, M) for f64 in (0, 1) for M in (4, 8, 11, 16, 21, 32)]
+
+HEADERS = ["nsw_device.cuh", "nsw_step.cuh", "nsw_registry.h", "nsw_ops.cuh"]
+
+
+def _nvcc():
+    for cand in (shutil.which("nvcc"), "/usr/local/cuda/bin/nvcc"):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _dep_mtime():
+    paths = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "nswrank_b200.h")]
+    return max(os.path.getmtime(p) for p in paths if os.path.exists(p))
+
+
+def _jobs():
+    jobs = []
+    for f64, M in INSTANCES:
+        tag = f"inst_{'f64' if f64 else 'f32'}_M{M}"
+        jobs.append((os.path.join(CSRC, "nsw_inst.cu"), os.path.join(BUILD, tag + ".o"),
+                     [f"-DNSW_F64={f64}", f"-DNSW_M={M}"]))
+    for name in ("nsw_common", "nsw_capi", "nsw_ops"):
+        jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(BUILD, name + ".o"), []))
+    return jobs
+
+
+def _compile(job, force, verbose):
+    src, obj, extra = job
+    if not force and os.path.exists(obj):
+        t = os.path.getmtime(obj)
+        if t > os.path.getmtime(src) and t > _dep_mtime():
+            return obj, "cached", ""
+    cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        raise RuntimeError(f"nvcc failed for {os.path.basename(obj)}:\n{p.stderr}")
+    return obj, "built", p.stderr
+
+
+def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
+    os.makedirs(BUILD, exist_ok=True)
+    work = _jobs()
+    n = jobs or max(1, min(len(work), os.cpu_count() or 4))
+    logs = []
+    with cf.ThreadPoolExecutor(max_workers=n) as ex:
+        for obj, status, log in ex.map(lambda j: _compile(j, force, verbose), work):
+            logs.append((obj, status, log))
+    objs = [o for o, _, _ in logs]
+    newest = max(os.path.getmtime(o) for o in objs)
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
+        tmp = LIB + ".tmp"
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
+        p = subprocess.run(cmd, capture_output=True, text=True)
+        if p.returncode != 0:
+            raise RuntimeError(f"link failed:\n{p.stderr}")
+        os.replace(tmp, LIB)
+    if verbose:
+        for obj, status, log in logs:
+            if status == "built":
+                print(f"== {os.path.basename(obj)}\n{log}")
+    return LIB
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("-j", type=int, default=None)
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    a = ap.parse_args(argv)
+    print(build(a.j, a.force, a.v))
+
+
+if __name__ == "__main__":
+    sys.exit(main())

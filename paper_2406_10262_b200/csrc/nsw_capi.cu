@@ -1,0 +1,667 @@
+// C ABI of libnswrank_b200.so (declared in include/nswrank_b200.h).
+//
+// Host runtime of the drop-in: owns the device state of one user shard,
+// chooses the fused-step tile variant, issues the per-step kernel sequence
+// (fused step -> impact reduction -> [caller's exchange] -> finalize),
+// captures it in a CUDA graph, and copies results back in the reference's
+// layouts.  Mirrors solve_fair_ranking (reference solver.py:138-241).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nswrank_b200.h"
+#include "nsw_registry.h"
+#include "nsw_step.cuh"
+
+namespace nsw {
+std::vector<Variant>& variant_registry() {
+  static std::vector<Variant> v;
+  return v;
+}
+}  // namespace nsw
+
+using namespace nsw;
+
+namespace {
+
+thread_local std::string g_err;
+
+nsw_status fail(nsw_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return fail(NSW_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+  } while (0)
+
+constexpr size_t kMaxSmem = 227 * 1024;
+
+int sizeof_dtype(int dt) { return dt == NSW_F64 ? 8 : 4; }
+
+// Pick the tile variant for (dtype, n, m, T): smallest M >= m, then the
+// smallest row capacity R*NT >= n (least padding), ties -> more rows per
+// thread (amortises the per-iteration column reduction).
+const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
+  auto& reg = variant_registry();
+  std::vector<const Variant*> c;
+  for (auto& v : reg)
+    if (v.dtype == dtype && v.M >= m && v.R * v.NT >= n && v.smem(T) <= kMaxSmem) c.push_back(&v);
+  if (c.empty()) return nullptr;
+  std::sort(c.begin(), c.end(), [](const Variant* a, const Variant* b) {
+    if (a->M != b->M) return a->M < b->M;
+    if (a->R * a->NT != b->R * b->NT) return a->R * a->NT < b->R * b->NT;
+    return a->R > b->R;
+  });
+  if (forced >= 0) {
+    // forced index counts over the candidates with the chosen M
+    std::vector<const Variant*> same;
+    for (auto* v : c)
+      if (v->M == c[0]->M) same.push_back(v);
+    if (forced < int(same.size())) return same[forced];
+  }
+  return c[0];
+}
+
+}  // namespace
+
+struct nsw_solver {
+  int dtype = 0;
+  int U = 0, n = 0, m = 0, T = 0, outer_max = 0, world = 1;
+  nsw_solver_config cfg{};
+  nsw_device_options opt{};
+  const Variant* var = nullptr;
+  size_t smem = 0;
+  int chunks = 1;
+  // device state
+  void *C = nullptr, *am = nullptr, *av = nullptr, *alpha = nullptr, *beta = nullptr, *hist = nullptr,
+       *xbest = nullptr, *rel = nullptr, *expo = nullptr;
+  double *expo_d = nullptr, *partial = nullptr, *split = nullptr, *imp_local = nullptr,
+         *imp_all = nullptr, *imp_cur = nullptr, *rel_sq = nullptr, *best = nullptr,
+         *objective = nullptr, *grad_norm = nullptr, *bc = nullptr;
+  unsigned long long* stamp = nullptr;
+  unsigned int* counter = nullptr;
+  int* state = nullptr;
+  int* state_host = nullptr;  // pinned
+  bool own_exchange = true;
+  double* own_imp_local = nullptr;
+  double* own_imp_all = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  bool graph_dirty = true;
+  int64_t launches = 0;
+  StepArgs<float> a32{};
+  StepArgs<double> a64{};
+  FinalizeArgs fin{};
+  float* flush_buf = nullptr;
+  size_t flush_n = 0;
+};
+
+namespace {
+
+template <typename S>
+void fill_step_args(nsw_solver* s, StepArgs<S>& a) {
+  a.U = s->U;
+  a.n = s->n;
+  a.m = s->m;
+  a.T = s->T;
+  a.outer_max = s->outer_max;
+  a.warm_start = s->cfg.warm_start;
+  a.C = (S*)s->C;
+  a.am = (S*)s->am;
+  a.av = (S*)s->av;
+  a.alpha = (S*)s->alpha;
+  a.beta = (S*)s->beta;
+  a.hist = (S*)s->hist;
+  a.xbest = (S*)s->xbest;
+  a.rel = (const S*)s->rel;
+  a.expo = (const S*)s->expo;
+  a.expo_d = s->expo_d;
+  a.partial = s->partial;
+  a.imp = s->imp_cur;
+  a.state = s->state;
+  a.bc = s->bc;
+  const double eps = s->cfg.epsilon;
+  a.nie = S(-1.0 / eps);
+  a.lr = S(s->cfg.adam_lr);
+  a.b1 = S(s->cfg.adam_beta1);
+  a.b2 = S(s->cfg.adam_beta2);
+  a.omb1 = S(1.0 - s->cfg.adam_beta1);
+  a.omb2 = S(1.0 - s->cfg.adam_beta2);
+  a.aeps = S(s->cfg.adam_eps);
+  const int n = s->n, m = s->m;
+  a.c_real = S(-eps * std::log(1.0 / n));
+  a.c_dummy = S(-eps * std::log(double(n - m + 1) / n));
+  a.mass_dummy = S(n - m + 1);
+  a.log_mass_dummy = S(std::log(double(n - m + 1)));
+}
+
+template <typename S>
+nsw_status upload_converted(void* dst, const double* src, size_t count) {
+  if constexpr (sizeof(S) == 8) {
+    CUDA_TRY(cudaMemcpy(dst, src, count * 8, cudaMemcpyHostToDevice));
+  } else {
+    std::vector<float> tmp(count);
+    for (size_t i = 0; i < count; ++i) tmp[i] = float(src[i]);
+    CUDA_TRY(cudaMemcpy(dst, tmp.data(), count * 4, cudaMemcpyHostToDevice));
+  }
+  return NSW_OK;
+}
+
+nsw_status download_converted(int dtype, const void* src, double* dst, size_t count) {
+  if (dtype == NSW_F64) {
+    CUDA_TRY(cudaMemcpy(dst, src, count * 8, cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<float> tmp(count);
+    CUDA_TRY(cudaMemcpy(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < count; ++i) dst[i] = double(tmp[i]);
+  }
+  return NSW_OK;
+}
+
+nsw_status validate_config(const nsw_solver_config* c) {
+  if (!c) return fail(NSW_ERR_ARG, "config is NULL");
+  if (!(c->epsilon > 0)) return fail(NSW_ERR_DOMAIN, "epsilon must be > 0");
+  if (!(c->sinkhorn_tol > 0)) return fail(NSW_ERR_DOMAIN, "sinkhorn_tol must be > 0");
+  if (!(c->grad_threshold > 0)) return fail(NSW_ERR_DOMAIN, "grad_threshold must be > 0");
+  if (c->sinkhorn_max_iters <= 0 || c->outer_max_iters <= 0)
+    return fail(NSW_ERR_DOMAIN, "iteration budgets must be positive");
+  return NSW_OK;
+}
+
+nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
+  void* args32[] = {&s->a32};
+  void* args64[] = {&s->a64};
+  CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
+                            s->smem, st));
+  const int bx = (s->n + 127) / 128;
+  impact_reduce_kernel<<<dim3(bx, s->chunks), 128, 0, st>>>(s->partial, s->U, s->n, s->chunks, s->split,
+                                                            s->imp_local, s->counter, s->state);
+  CUDA_TRY(cudaGetLastError());
+  s->launches += 2;
+  return NSW_OK;
+}
+
+nsw_status launch_finalize(nsw_solver* s, cudaStream_t st) {
+  finalize_kernel<<<1, 512, 0, st>>>(s->fin);
+  CUDA_TRY(cudaGetLastError());
+  s->launches += 1;
+  return NSW_OK;
+}
+
+nsw_status refresh_args(nsw_solver* s) {
+  fill_step_args(s, s->a32);
+  fill_step_args(s, s->a64);
+  s->fin.n = s->n;
+  s->fin.world = s->world;
+  s->fin.outer_max = s->outer_max;
+  s->fin.imp_all = s->imp_all;
+  s->fin.rel_sq = s->rel_sq;
+  s->fin.grad_threshold = s->cfg.grad_threshold;
+  s->fin.imp_cur = s->imp_cur;
+  s->fin.best = s->best;
+  s->fin.objective = s->objective;
+  s->fin.grad_norm = s->grad_norm;
+  s->fin.stamp = s->stamp;
+  s->fin.state = s->state;
+  s->graph_dirty = true;
+  return NSW_OK;
+}
+
+nsw_status read_state(nsw_solver* s) {
+  CUDA_TRY(cudaMemcpyAsync(s->state_host, s->state, 4 * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return NSW_OK;
+}
+
+template <typename T>
+nsw_status dmalloc(T** p, size_t bytes) {
+  CUDA_TRY(cudaMalloc((void**)p, std::max<size_t>(bytes, 16)));
+  CUDA_TRY(cudaMemset(*p, 0, std::max<size_t>(bytes, 16)));
+  return NSW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nsw_last_error(void) { return g_err.c_str(); }
+const char* nsw_version(void) { return "nswrank_b200 0.1.0 (sm_100a)"; }
+
+int32_t nsw_supported(int32_t dtype, int32_t n, int32_t m, int32_t iters) {
+  return choose_variant(dtype, n, m, iters, -1) != nullptr;
+}
+
+nsw_status nsw_solver_create(const double* relevance_local, const double* exposure, int32_t users_local,
+                             int32_t n, int32_t m, const double* rel_sq_sum, int32_t world,
+                             const nsw_solver_config* config, const nsw_device_options* options,
+                             nsw_solver** out) {
+  if (!out || !relevance_local || !exposure || !options) return fail(NSW_ERR_ARG, "NULL argument");
+  *out = nullptr;
+  nsw_status st = validate_config(config);
+  if (st != NSW_OK) return st;
+  if (users_local <= 0 || n <= 0 || m < 2 || m > n)
+    return fail(NSW_ERR_SHAPE, "need users > 0 and 2 <= num_positions <= num_items");
+  if (world < 1) return fail(NSW_ERR_ARG, "world must be >= 1");
+  if (options->dtype != NSW_F32 && options->dtype != NSW_F64) return fail(NSW_ERR_ARG, "bad dtype");
+  if (options->schedule != NSW_SCHEDULE_FIXED)
+    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is not implemented on the device yet");
+  const int T = config->sinkhorn_max_iters;
+  const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
+  if (!var)
+    return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +
+                                         " n=" + std::to_string(n) + " m=" + std::to_string(m) +
+                                         " T=" + std::to_string(T));
+  CUDA_TRY(cudaSetDevice(options->device));
+  auto* s = new nsw_solver();
+  s->dtype = options->dtype;
+  s->U = users_local;
+  s->n = n;
+  s->m = m;
+  s->T = T;
+  s->outer_max = config->outer_max_iters;
+  s->world = world;
+  s->cfg = *config;
+  s->opt = *options;
+  if (s->opt.check_every <= 0) s->opt.check_every = 8;
+  s->var = var;
+  s->smem = var->smem(T);
+  {
+    // user chunks of the impact reduction: ~2 CTAs per SM in total
+    const int bx = (n + 127) / 128;
+    s->chunks = std::max(1, std::min(users_local, (2 * 148 + bx - 1) / bx));
+  }
+  const size_t es = sizeof_dtype(s->dtype);
+  const size_t cells = size_t(users_local) * n * m;
+  nsw_status e = NSW_OK;
+#define ALLOC(p, bytes)                       \
+  do {                                        \
+    e = dmalloc(&(p), (bytes));               \
+    if (e != NSW_OK) {                        \
+      nsw_solver_destroy(s);                  \
+      return e;                               \
+    }                                         \
+  } while (0)
+  ALLOC(s->C, cells * es);
+  ALLOC(s->am, cells * es);
+  ALLOC(s->av, cells * es);
+  ALLOC(s->xbest, cells * es);
+  ALLOC(s->alpha, size_t(users_local) * n * es);
+  ALLOC(s->beta, size_t(users_local) * m * es);
+  ALLOC(s->hist, size_t(users_local) * (T + 1) * m * es);
+  ALLOC(s->rel, size_t(users_local) * n * es);
+  ALLOC(s->expo, size_t(m) * es);
+  ALLOC(s->expo_d, size_t(m) * 8);
+  ALLOC(s->partial, size_t(users_local) * n * 8);
+  ALLOC(s->split, size_t(s->chunks) * n * 8);
+  ALLOC(s->own_imp_local, size_t(n) * 8);
+  ALLOC(s->own_imp_all, size_t(world) * n * 8);
+  ALLOC(s->imp_cur, size_t(n) * 8);
+  ALLOC(s->rel_sq, size_t(n) * 8);
+  ALLOC(s->best, 8);
+  ALLOC(s->objective, size_t(s->outer_max) * 8);
+  ALLOC(s->grad_norm, size_t(s->outer_max) * 8);
+  ALLOC(s->bc, size_t(2) * (s->outer_max + 1) * 8);
+  ALLOC(s->stamp, size_t(s->outer_max + 1) * 8);
+  ALLOC(s->counter, 16);
+  ALLOC(s->state, 16);
+#undef ALLOC
+  s->imp_local = s->own_imp_local;
+  s->imp_all = world == 1 ? s->own_imp_local : s->own_imp_all;
+  if (cudaMallocHost((void**)&s->state_host, 16) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "cudaMallocHost failed");
+  }
+  if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "cudaStreamCreate failed");
+  }
+  if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");
+  }
+  // inputs
+  if ((e = s->dtype == NSW_F64 ? upload_converted<double>(s->rel, relevance_local, size_t(users_local) * n)
+                              : upload_converted<float>(s->rel, relevance_local, size_t(users_local) * n)) !=
+      NSW_OK) {
+    nsw_solver_destroy(s);
+    return e;
+  }
+  std::vector<double> ex(m, 0.0);
+  double exp_sq = 0.0;
+  for (int k = 0; k < m - 1; ++k) {
+    ex[k] = exposure[k];
+    exp_sq += exposure[k] * exposure[k];
+  }
+  if ((e = s->dtype == NSW_F64 ? upload_converted<double>(s->expo, ex.data(), m)
+                              : upload_converted<float>(s->expo, ex.data(), m)) != NSW_OK) {
+    nsw_solver_destroy(s);
+    return e;
+  }
+  std::vector<double> rsq(n, 0.0);
+  if (rel_sq_sum) {
+    for (int i = 0; i < n; ++i) rsq[i] = rel_sq_sum[i];
+  } else {
+    for (int u = 0; u < users_local; ++u)
+      for (int i = 0; i < n; ++i) rsq[i] += relevance_local[size_t(u) * n + i] * relevance_local[size_t(u) * n + i];
+  }
+  // Adam bias corrections exactly as the reference computes them (Python
+  // floats: 1.0 - b1**step, solver.py:118-119).
+  std::vector<double> bc(size_t(2) * (s->outer_max + 1), 1.0);
+  for (int st2 = 1; st2 <= s->outer_max; ++st2) {
+    bc[2 * st2] = 1.0 - std::pow(config->adam_beta1, double(st2));
+    bc[2 * st2 + 1] = 1.0 - std::pow(config->adam_beta2, double(st2));
+  }
+  const double neg_inf = -INFINITY;
+  int init_state[4] = {PHASE_INIT, 0, 0, 0};
+  if (cudaMemcpy(s->expo_d, ex.data(), m * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(s->rel_sq, rsq.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(s->bc, bc.data(), bc.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(s->best, &neg_inf, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(s->state, init_state, sizeof(init_state), cudaMemcpyHostToDevice) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "initial upload failed");
+  }
+  s->fin.exp_sq = exp_sq;
+  refresh_args(s);
+  stamp_kernel<<<1, 1, 0, s->stream>>>(s->stamp);
+  s->launches += 1;
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "stream sync failed");
+  }
+  *out = s;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_destroy(nsw_solver* s) {
+  if (!s) return NSW_OK;
+  if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
+                  s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
+                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  if (s->state_host) cudaFreeHost(s->state_host);
+  if (s->stream) cudaStreamDestroy(s->stream);
+  delete s;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_exchange_buffers(nsw_solver* s, void** local_dev, void** gathered_dev) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  if (local_dev) *local_dev = s->imp_local;
+  if (gathered_dev) *gathered_dev = s->imp_all;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_bind_exchange(nsw_solver* s, void* local_dev, void* gathered_dev) {
+  if (!s || !local_dev || !gathered_dev) return fail(NSW_ERR_ARG, "NULL argument");
+  s->imp_local = (double*)local_dev;
+  s->imp_all = (double*)gathered_dev;
+  return refresh_args(s);
+}
+
+nsw_status nsw_solver_local_step(nsw_solver* s, void* stream) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  return launch_step(s, stream ? (cudaStream_t)stream : s->stream);
+}
+
+nsw_status nsw_solver_finalize(nsw_solver* s, void* stream) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  return launch_finalize(s, stream ? (cudaStream_t)stream : s->stream);
+}
+
+static nsw_status ensure_graph(nsw_solver* s) {
+  if (!s->graph_dirty && s->gexec) return NSW_OK;
+  if (s->gexec) {
+    cudaGraphExecDestroy(s->gexec);
+    s->gexec = nullptr;
+  }
+  cudaGraph_t g;
+  CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t before = s->launches;
+  nsw_status e = launch_step(s, s->stream);
+  if (e == NSW_OK) e = launch_finalize(s, s->stream);
+  s->launches = before;
+  cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+  if (e != NSW_OK) return e;
+  if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  ce = cudaGraphInstantiate(&s->gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  s->graph_dirty = false;
+  return NSW_OK;
+}
+
+static nsw_status one_step(nsw_solver* s) {
+  if (s->opt.use_graph) {
+    nsw_status e = ensure_graph(s);
+    if (e != NSW_OK) return e;
+    CUDA_TRY(cudaGraphLaunch(s->gexec, s->stream));
+    s->launches += 3;
+    return NSW_OK;
+  }
+  nsw_status e = launch_step(s, s->stream);
+  if (e != NSW_OK) return e;
+  return launch_finalize(s, s->stream);
+}
+
+nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  if (s->world != 1) return fail(NSW_ERR_ARG, "nsw_solver_run drives a single shard (world == 1)");
+  if (done) *done = 0;
+  for (int it = 0; it < max_steps; ++it) {
+    nsw_status e = one_step(s);
+    if (e != NSW_OK) return e;
+    if ((it + 1) % s->opt.check_every == 0 || it + 1 == max_steps) {
+      e = read_state(s);
+      if (e != NSW_OK) return e;
+      if (s->state_host[ST_PHASE] == PHASE_FINISHED) {
+        if (done) *done = 1;
+        break;
+      }
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_status(nsw_solver* s, int32_t* phase, int32_t* steps, int32_t* errors) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  nsw_status e = read_state(s);
+  if (e != NSW_OK) return e;
+  if (phase) *phase = s->state_host[ST_PHASE];
+  if (steps) *steps = s->state_host[ST_STEP];
+  if (errors) *errors = s->state_host[ST_ERR];
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_stream(nsw_solver* s, void** stream) {
+  if (!s || !stream) return fail(NSW_ERR_ARG, "NULL argument");
+  *stream = s->stream;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  CUDA_TRY(cudaDeviceSynchronize());
+  nsw_status e = read_state(s);
+  if (e != NSW_OK) return e;
+  const int steps = s->state_host[ST_STEP];
+  if (policy_out) {
+    e = download_converted(s->dtype, s->xbest, policy_out, size_t(s->U) * s->n * s->m);
+    if (e != NSW_OK) return e;
+  }
+  if (trace) {
+    trace->steps = steps;
+    std::vector<unsigned long long> st(steps + 1);
+    if (steps > 0) {
+      if (trace->objective) CUDA_TRY(cudaMemcpy(trace->objective, s->objective, steps * 8, cudaMemcpyDeviceToHost));
+      if (trace->grad_norm) CUDA_TRY(cudaMemcpy(trace->grad_norm, s->grad_norm, steps * 8, cudaMemcpyDeviceToHost));
+      CUDA_TRY(cudaMemcpy(st.data(), s->stamp, (steps + 1) * 8, cudaMemcpyDeviceToHost));
+    }
+    for (int k = 0; k < steps; ++k) {
+      if (trace->sinkhorn_iterations) trace->sinkhorn_iterations[k] = s->T;
+      if (trace->wall_time) trace->wall_time[k] = double(st[k + 1] - st[k]) * 1e-9;
+    }
+  }
+  const int err = s->state_host[ST_ERR];
+  if (err & ERR_IMPACT) return fail(NSW_ERR_DOMAIN, "item impact became nonpositive during the solve");
+  return NSW_OK;
+}
+
+static nsw_status field_ptr(nsw_solver* s, const char* f, void** p, size_t* count, bool* typed) {
+  const size_t cells = size_t(s->U) * s->n * s->m;
+  *typed = true;
+  if (!strcmp(f, "cost")) { *p = s->C; *count = cells; }
+  else if (!strcmp(f, "adam_m")) { *p = s->am; *count = cells; }
+  else if (!strcmp(f, "adam_v")) { *p = s->av; *count = cells; }
+  else if (!strcmp(f, "xbest")) { *p = s->xbest; *count = cells; }
+  else if (!strcmp(f, "alpha")) { *p = s->alpha; *count = size_t(s->U) * s->n; }
+  else if (!strcmp(f, "beta") || !strcmp(f, "lvi")) { *p = s->beta; *count = size_t(s->U) * s->m; }
+  else if (!strcmp(f, "hist")) { *p = s->hist; *count = size_t(s->U) * (s->T + 1) * s->m; }
+  else if (!strcmp(f, "partial")) { *p = s->partial; *count = size_t(s->U) * s->n; *typed = false; }
+  else if (!strcmp(f, "imp")) { *p = s->imp_cur; *count = s->n; *typed = false; }
+  else if (!strcmp(f, "imp_local")) { *p = s->imp_local; *count = s->n; *typed = false; }
+  else if (!strcmp(f, "objective")) { *p = s->objective; *count = s->outer_max; *typed = false; }
+  else if (!strcmp(f, "grad_norm")) { *p = s->grad_norm; *count = s->outer_max; *typed = false; }
+  else return fail(NSW_ERR_ARG, std::string("unknown field ") + f);
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t count) {
+  if (!s || !field || !host) return fail(NSW_ERR_ARG, "NULL argument");
+  void* p;
+  size_t c;
+  bool typed;
+  nsw_status e = field_ptr(s, field, &p, &c, &typed);
+  if (e != NSW_OK) return e;
+  if (count != c) return fail(NSW_ERR_SHAPE, std::string("field ") + field + " has " + std::to_string(c) + " elements");
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (!typed) {
+    CUDA_TRY(cudaMemcpy(host, p, c * 8, cudaMemcpyDeviceToHost));
+    return NSW_OK;
+  }
+  return download_converted(s->dtype, p, host, c);
+}
+
+nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, size_t count) {
+  if (!s || !field || !host) return fail(NSW_ERR_ARG, "NULL argument");
+  void* p;
+  size_t c;
+  bool typed;
+  nsw_status e = field_ptr(s, field, &p, &c, &typed);
+  if (e != NSW_OK) return e;
+  if (count != c) return fail(NSW_ERR_SHAPE, std::string("field ") + field + " has " + std::to_string(c) + " elements");
+  CUDA_TRY(cudaDeviceSynchronize());
+  if (!typed) {
+    CUDA_TRY(cudaMemcpy(p, host, c * 8, cudaMemcpyHostToDevice));
+    return NSW_OK;
+  }
+  return s->dtype == NSW_F64 ? upload_converted<double>(p, host, c) : upload_converted<float>(p, host, c);
+}
+
+nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value) {
+  if (!s || !field) return fail(NSW_ERR_ARG, "NULL argument");
+  CUDA_TRY(cudaDeviceSynchronize());
+  int idx = -1;
+  if (!strcmp(field, "phase")) idx = ST_PHASE;
+  else if (!strcmp(field, "step")) idx = ST_STEP;
+  else if (!strcmp(field, "improved")) idx = ST_IMPROVED;
+  if (idx >= 0) {
+    int v = int(value);
+    CUDA_TRY(cudaMemcpy(s->state + idx, &v, 4, cudaMemcpyHostToDevice));
+    return NSW_OK;
+  }
+  if (!strcmp(field, "best_is_neg_inf")) {
+    const double neg_inf = -INFINITY;
+    CUDA_TRY(cudaMemcpy(s->best, &neg_inf, 8, cudaMemcpyHostToDevice));
+    return NSW_OK;
+  }
+  return fail(NSW_ERR_ARG, std::string("unknown scalar ") + field);
+}
+
+int64_t nsw_solver_launch_count(nsw_solver* s) { return s ? s->launches : -1; }
+
+nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT, int32_t* smem) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  if (M) *M = s->var->M;
+  if (R) *R = s->var->R;
+  if (NT) *NT = s->var->NT;
+  if (smem) *smem = int(s->smem);
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
+                                 float* ms_fused) {
+  if (!s || steps <= 0) return fail(NSW_ERR_ARG, "bad arguments");
+  if (s->world != 1) return fail(NSW_ERR_ARG, "timing helper drives a single shard");
+  if (flush_l2 && !s->flush_buf) {
+    s->flush_n = size_t(256) << 20;  // 1 GiB of floats > 126 MB L2
+    CUDA_TRY(cudaMalloc((void**)&s->flush_buf, s->flush_n * 4));
+    CUDA_TRY(cudaMemset(s->flush_buf, 0, s->flush_n * 4));
+  }
+  std::vector<cudaEvent_t> ev(size_t(3) * steps);
+  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
+  for (int i = 0; i < steps; ++i) {
+    if (flush_l2) {
+      flush_kernel<<<148 * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaEventRecord(ev[3 * i], s->stream));
+    void* args32[] = {&s->a32};
+    void* args64[] = {&s->a64};
+    CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT),
+                              s->dtype == NSW_F64 ? args64 : args32, s->smem, s->stream));
+    CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
+    const int bx = (s->n + 127) / 128;
+    impact_reduce_kernel<<<dim3(bx, s->chunks), 128, 0, s->stream>>>(s->partial, s->U, s->n, s->chunks,
+                                                                       s->split, s->imp_local, s->counter,
+                                                                       s->state);
+    finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));
+    s->launches += 3;
+  }
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  float tot = 0.f, fus = 0.f;
+  for (int i = 0; i < steps; ++i) {
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
+    CUDA_TRY(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 1]));
+    tot += a;
+    fus += b;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (ms_total) *ms_total = tot;
+  if (ms_fused) *ms_fused = fus;
+  return NSW_OK;
+}
+
+nsw_status nsw_solve_fair_ranking(const double* relevance, const double* exposure, int32_t U, int32_t n,
+                                  int32_t m, const nsw_solver_config* config,
+                                  const nsw_device_options* options, double* policy_out, nsw_trace* trace) {
+  if (!relevance || !exposure || !config || !options) return fail(NSW_ERR_ARG, "NULL argument");
+  nsw_solver* s = nullptr;
+  nsw_status e = nsw_solver_create(relevance, exposure, U, n, m, nullptr, 1, config, options, &s);
+  if (e != NSW_OK) return e;
+  // at most outer_max forwards + one materialisation step
+  int32_t done = 0;
+  e = nsw_solver_run(s, config->outer_max_iters + 1, &done);
+  if (e == NSW_OK) e = nsw_solver_result(s, policy_out, trace);
+  if (e == NSW_OK && !done) e = fail(NSW_ERR_STATE, "solver did not reach its stop state");
+  nsw_solver_destroy(s);
+  return e;
+}
+
+}  // extern "C"

@@ -1,0 +1,188 @@
+// Device building blocks of the NSW ascent path (sm_100a).
+//
+// Data layout in HBM (per GPU, users are this rank's contiguous block):
+//   C, adam_m, adam_v, xbest : [U][n][m]   reference layout (solver.py:176-185)
+//   alpha                    : [U][n]      row dual after inner iteration 1
+//   beta                     : [U][m]      column dual after inner iteration 1
+//   hist                     : [U][T+1][m] v~^t = exp(v^t - beta), t = 0..T
+//   partial                  : [U][n] f64  per-user impact terms
+//
+// Numerical form ("stabilised multiplicative"):
+// iteration 1 of every solve runs in the log domain exactly like the
+// reference (sinkhorn.py:219-234); its duals (alpha, beta) are absorbed into
+// K~ = exp(K + alpha 1' + 1 beta') = X^1, a properly scaled plan in [0, 1],
+// and iterations 2..T are u~ = 1/(K~ v~), v~ = colmass/(K~' u~) -- two FMAs
+// per cell and one reciprocal per row / column, with K~ held in registers.
+// The unrolled reverse mode (sinkhorn.py:258-309) is restated in the same
+// coordinates (see step_kernel below).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+namespace nsw {
+
+// PHASE_RESUME: forward of step k from a caller-provided cost tensor, with the
+// warm-start duals lvi supplied in the `beta` buffer (checkpoint / resume,
+// and one-step parity from an oracle state).
+enum : int { PHASE_INIT = 0, PHASE_RUNNING = 1, PHASE_DONE_PENDING = 2, PHASE_FINISHED = 3, PHASE_RESUME = 4 };
+enum : int { ST_PHASE = 0, ST_STEP = 1, ST_IMPROVED = 2, ST_ERR = 3 };
+enum : int { ERR_IMPACT = 1, ERR_NONFINITE = 2 };
+
+template <typename S>
+struct Fp;
+
+template <>
+struct Fp<float> {
+  static __device__ __forceinline__ float exp_(float x) { return expf(x); }
+  static __device__ __forceinline__ float log_(float x) { return logf(x); }
+  static __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+  static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float sqrt_(float x) { return __fsqrt_rn(x); }
+  static __device__ __forceinline__ float ninf() { return -CUDART_INF_F; }
+  static constexpr int kVec = 4;  // elements per 16-byte vector
+};
+
+template <>
+struct Fp<double> {
+  static __device__ __forceinline__ double exp_(double x) { return exp(x); }
+  static __device__ __forceinline__ double log_(double x) { return log(x); }
+  static __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+  static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double sqrt_(double x) { return __dsqrt_rn(x); }
+  static __device__ __forceinline__ double ninf() { return -CUDART_INF; }
+  static constexpr int kVec = 2;
+};
+
+// Padded row pitch (elements) of a K~ row in shared memory: 16-byte multiple.
+template <typename S, int M>
+struct Pitch {
+  static constexpr int value = (M + Fp<S>::kVec - 1) / Fp<S>::kVec * Fp<S>::kVec;
+};
+
+struct OpSum {
+  template <typename S>
+  __device__ __forceinline__ S operator()(S a, S b) const { return a + b; }
+  template <typename S>
+  static __device__ __forceinline__ S identity() { return S(0); }
+};
+
+struct OpMax {
+  template <typename S>
+  __device__ __forceinline__ S operator()(S a, S b) const { return a > b ? a : b; }
+  template <typename S>
+  static __device__ __forceinline__ S identity() { return Fp<S>::ninf(); }
+};
+
+// Warp reduce-scatter of an M-vector held by every lane.  Stage OFF halves
+// the live range: the lane with bit OFF clear keeps the lower half, its
+// partner the upper half, each receiving the other's copy of its half.
+// Cost ~ M shuffles instead of 5*M for a full butterfly.  After the five
+// stages lane L holds the warp totals of columns [base, base+ceil(M/32))
+// clipped at `lim` (columns past `lim` are padding of an uneven split).
+template <typename S, int M, int CNT, int OFF, class Op>
+__device__ __forceinline__ void reduce_scatter(S (&v)[M], int lane, int& base, int& lim) {
+  if constexpr (OFF > 0) {
+    constexpr int H = (CNT + 1) / 2;
+    const bool up = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const S lo = v[j];
+      const S hi = (j + H < CNT) ? v[(j + H < CNT) ? (j + H) : 0] : Op::template identity<S>();
+      const S send = up ? lo : hi;
+      const S keep = up ? hi : lo;
+      v[j] = Op{}(keep, __shfl_xor_sync(0xffffffffu, send, OFF));
+    }
+    if (up) {
+      base += H;
+    } else {
+      lim = min(lim, base + H);
+    }
+    reduce_scatter<S, M, H, OFF / 2, Op>(v, lane, base, lim);
+  }
+}
+
+// Column reduction of per-thread M-vectors over the whole CTA, in a fixed
+// order (warp reduce-scatter, then warps summed in index order by thread k),
+// so results are bitwise deterministic.  fin(k, total) runs on thread k < m
+// between the two barriers.  `v` is destroyed.
+template <typename S, int M, int NT, class Op, class Fin>
+__device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fin) {
+  constexpr int NW = NT / 32;
+  constexpr int CF = (M + 31) / 32;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  int base = 0, lim = M;
+  reduce_scatter<S, M, M, 16, Op>(v, lane, base, lim);
+#pragma unroll
+  for (int j = 0; j < CF; ++j) {
+    const int col = base + j;
+    if (col < lim && col < m) red[warp * M + col] = v[j];
+  }
+  __syncthreads();
+  if (threadIdx.x < m) {
+    const int k = threadIdx.x;
+    S acc = red[k];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) acc = Op{}(acc, red[w * M + k]);
+    fin(k, acc);
+  }
+  __syncthreads();
+}
+
+// Load an M-vector from shared memory (16-byte vector loads; pitch padded).
+template <typename S, int M>
+__device__ __forceinline__ void lds_vec(S (&dst)[M], const S* src) {
+  constexpr int V = Fp<S>::kVec;
+  if constexpr (V == 4) {
+#pragma unroll
+    for (int q = 0; q < (M + 3) / 4; ++q) {
+      const float4 t = reinterpret_cast<const float4*>(src)[q];
+      if (4 * q + 0 < M) dst[(4 * q + 0 < M) ? 4 * q + 0 : 0] = t.x;
+      if (4 * q + 1 < M) dst[(4 * q + 1 < M) ? 4 * q + 1 : 0] = t.y;
+      if (4 * q + 2 < M) dst[(4 * q + 2 < M) ? 4 * q + 2 : 0] = t.z;
+      if (4 * q + 3 < M) dst[(4 * q + 3 < M) ? 4 * q + 3 : 0] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < (M + 1) / 2; ++q) {
+      const double2 t = reinterpret_cast<const double2*>(src)[q];
+      if (2 * q + 0 < M) dst[(2 * q + 0 < M) ? 2 * q + 0 : 0] = t.x;
+      if (2 * q + 1 < M) dst[(2 * q + 1 < M) ? 2 * q + 1 : 0] = t.y;
+    }
+  }
+}
+
+template <typename S, int M>
+__device__ __forceinline__ void sts_vec(S* dst, const S (&src)[M]) {
+  constexpr int V = Fp<S>::kVec;
+  constexpr int P = Pitch<S, M>::value;
+  if constexpr (V == 4) {
+#pragma unroll
+    for (int q = 0; q < P / 4; ++q) {
+      float4 t;
+      t.x = (4 * q + 0 < M) ? src[(4 * q + 0 < M) ? 4 * q + 0 : 0] : 0.f;
+      t.y = (4 * q + 1 < M) ? src[(4 * q + 1 < M) ? 4 * q + 1 : 0] : 0.f;
+      t.z = (4 * q + 2 < M) ? src[(4 * q + 2 < M) ? 4 * q + 2 : 0] : 0.f;
+      t.w = (4 * q + 3 < M) ? src[(4 * q + 3 < M) ? 4 * q + 3 : 0] : 0.f;
+      reinterpret_cast<float4*>(dst)[q] = t;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < P / 2; ++q) {
+      double2 t;
+      t.x = (2 * q + 0 < M) ? src[(2 * q + 0 < M) ? 2 * q + 0 : 0] : 0.0;
+      t.y = (2 * q + 1 < M) ? src[(2 * q + 1 < M) ? 2 * q + 1 : 0] : 0.0;
+      reinterpret_cast<double2*>(dst)[q] = t;
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+}  // namespace nsw

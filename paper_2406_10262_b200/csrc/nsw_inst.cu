@@ -1,0 +1,71 @@
+// One translation unit per (scalar type, M): compiled with
+//   -DNSW_F64=0|1 -DNSW_M=<columns>
+// and registers the (rows/thread, threads/CTA) tile shapes for that pair.
+#include "nsw_registry.h"
+#include "nsw_step.cuh"
+
+#ifndef NSW_M
+#error "NSW_M must be defined"
+#endif
+#if NSW_F64
+#define NSW_S double
+#define NSW_DT 1
+#else
+#define NSW_S float
+#define NSW_DT 0
+#endif
+
+namespace nsw {
+namespace {
+
+template <int R, int NT>
+size_t smem_of(int T) {
+  return step_smem_bytes<NSW_S, NSW_M, R, NT>(T);
+}
+
+#define NSW_CAT2(a, b) a##b
+#define NSW_CAT(a, b) NSW_CAT2(a, b)
+#define NSW_REG(R, NT)                                                                        \
+  Registrar NSW_CAT(reg_, __LINE__)(Variant{NSW_DT, NSW_M, R, NT,                             \
+                                            (const void*)&step_kernel<NSW_S, NSW_M, R, NT>, \
+                                            &smem_of<R, NT>});
+
+#if NSW_F64
+#if NSW_M <= 16
+NSW_REG(1, 64)
+NSW_REG(1, 128)
+NSW_REG(1, 256)
+NSW_REG(2, 256)
+NSW_REG(2, 512)
+#else
+NSW_REG(1, 64)
+NSW_REG(1, 128)
+NSW_REG(1, 256)
+NSW_REG(1, 512)
+#endif
+#else
+#if NSW_M <= 16
+NSW_REG(1, 64)
+NSW_REG(2, 64)
+NSW_REG(4, 64)
+NSW_REG(8, 64)
+NSW_REG(4, 128)
+NSW_REG(8, 128)
+NSW_REG(8, 256)
+#elif NSW_M <= 24
+NSW_REG(1, 64)
+NSW_REG(2, 64)
+NSW_REG(4, 64)
+NSW_REG(4, 128)
+NSW_REG(4, 256)
+#else
+NSW_REG(1, 64)
+NSW_REG(2, 64)
+NSW_REG(2, 128)
+NSW_REG(2, 256)
+NSW_REG(2, 512)
+#endif
+#endif
+
+}  // namespace
+}  // namespace nsw

@@ -1,0 +1,437 @@
+// Fused outer-step kernel of the NSW ascent:  [backward of step k-1 +
+// Adam ascent on the cost tile +] forward of step k + per-item impact terms.
+//
+// One CTA per user.  Replaces, per user, reference solver.py:186-240 minus
+// the cross-user impact sum (solver.py:206), which is the only coupling
+// between users and is done by impact_reduce_kernel / finalize_kernel.
+//
+// Register / shared-memory residency:
+//   forward : K~ (R rows x M columns per thread) in registers; the column
+//             scaling vector and the v~ history in shared memory.
+//   backward: G (the K~-coordinates adjoint, R x M per thread) in registers,
+//             K~ in shared memory (one 16-byte-vector row read per level).
+#pragma once
+
+#include "nsw_device.cuh"
+
+namespace nsw {
+
+template <typename S>
+struct StepArgs {
+  int U, n, m, T, outer_max, warm_start;
+  S* C;          // [U][n][m] transport costs (the ascent variable)
+  S* am;         // [U][n][m] Adam first moment
+  S* av;         // [U][n][m] Adam second moment
+  S* alpha;      // [U][n]    row dual after inner iteration 1 (absorption point)
+  S* beta;       // [U][m]    column dual after inner iteration 1
+  S* hist;       // [U][T+1][m] v~^t, t = 0..T  (v~^0 = exp(lvi - beta), v~^1 = 1)
+  S* xbest;      // [U][n][m] best-F policy so far
+  const S* rel;          // [U][n]
+  const S* expo;         // [m-1]
+  const double* expo_d;  // [m-1] (impact terms are accumulated in float64)
+  double* partial;       // [U][n] sum_{k<m-1} r_ui e_k x_uik
+  const double* imp;     // [n] Imp of the step being differentiated
+  const int* state;      // device step state (ST_*)
+  const double* bc;      // [2*(outer_max+1)] Adam bias corrections 1-b1^s, 1-b2^s
+  S nie;                 // -1/eps (solver.py:188, :236)
+  S lr, b1, b2, omb1, omb2, aeps;
+  S c_real, c_dummy;     // initial costs -eps*log(1/n), -eps*log((n-m+1)/n)
+  S mass_dummy, log_mass_dummy;
+};
+
+template <typename S>
+__device__ __forceinline__ S mul_(S a, S b);
+template <>
+__device__ __forceinline__ float mul_(float a, float b) { return __fmul_rn(a, b); }
+template <>
+__device__ __forceinline__ double mul_(double a, double b) { return __dmul_rn(a, b); }
+template <typename S>
+__device__ __forceinline__ S add_(S a, S b);
+template <>
+__device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b); }
+template <>
+__device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename S, int M>
+__device__ __forceinline__ S row_dot(const S (&x)[M], const S (&y)[M]) {
+  S s = S(0);
+#pragma unroll
+  for (int k = 0; k < M; ++k) s = fma(x[k], y[k], s);
+  return s;
+}
+
+template <typename S, int M>
+__device__ __forceinline__ S row_dot2(const S* x, const S (&y)[M]) {
+  S s = S(0);
+#pragma unroll
+  for (int k = 0; k < M; ++k) s = fma(x[k], y[k], s);
+  return s;
+}
+
+template <typename S, int M, int R, int NT>
+__host__ __device__ constexpr size_t step_smem_bytes(int T) {
+  constexpr int P = Pitch<S, M>::value;
+  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + size_t(NT) * R);
+}
+
+template <typename S, int M, int R, int NT>
+__global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
+  using F = Fp<S>;
+  constexpr int P = Pitch<S, M>::value;
+  constexpr int NW = NT / 32;
+  static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = a.T;
+  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K~ rows (backward)
+  S* vh = Kt + size_t(NT) * R * P;          // [T+1][P]   v~ history
+  S* red = vh + size_t(T + 1) * P;          // [NW][P]    column partials
+  S* vec0 = red + NW * P;                   // [P] scaling vector / cv
+  S* vec1 = vec0 + P;                       // [P] beta / column max
+  S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
+  S* utT_s = vec2 + P;                      // [NT*R] u~^T per row
+
+  const int phase = a.state[ST_PHASE];
+  if (phase == PHASE_FINISHED) return;
+
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int n = a.n, m = a.m;
+  const size_t ubase = size_t(u) * n * m;
+  S* Cu = a.C + ubase;
+  S* mu = a.am + ubase;
+  S* vu = a.av + ubase;
+  S* xb = a.xbest + ubase;
+  S* hu = a.hist + size_t(u) * (T + 1) * m;
+
+  auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
+  auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
+
+  if (tid < P) {
+    vec0[tid] = S(0);
+    vec1[tid] = S(0);
+    vec2[tid] = S(0);
+  }
+
+  S A[R][M];  // forward: K~ ; backward: adjoint G  (gK = W + K~ .* G)
+  S ut[R];    // current u~ per row
+
+  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
+    // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
+    __syncthreads();
+    if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
+    for (int idx = tid; idx < (T + 1) * P; idx += NT) {
+      const int t = idx / P, k = idx - t * P;
+      vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
+    }
+    __syncthreads();
+    S bt[M], vT1[M], vT[M];
+    lds_vec<S, M>(bt, vec1);
+    lds_vec<S, M>(vT, vh + size_t(T) * P);
+    if (T >= 2) lds_vec<S, M>(vT1, vh + size_t(T - 1) * P);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      S kr[M];
+      const S al = i < n ? a.alpha[size_t(u) * n + i] : S(0);
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        kr[k] = (i < n && k < m) ? F::exp_(add_(add_(mul_(Cu[size_t(i) * m + k], a.nie), al), bt[k])) : S(0);
+      sts_vec<S, M>(Kt + size_t(i) * P, kr);
+      S uT = S(0);
+      if (i < n) uT = (T >= 2) ? F::rcp(row_dot<S, M>(kr, vT1)) : S(1);
+      utT_s[i] = uT;
+      ut[r] = uT;
+    }
+    const int improved = a.state[ST_IMPROVED];
+    if (phase == PHASE_DONE_PENDING) {
+      // the stop fired after step k-1's forward: only its policy is still owed
+      if (improved) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          if (i >= n) continue;
+          const S* kr = Kt + size_t(i) * P;
+          for (int k = 0; k < m; ++k) xb[size_t(i) * m + k] = mul_(mul_(kr[k], ut[r]), vT[k]);
+        }
+      }
+      return;
+    }
+
+    // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
+    S ex[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
+    S c[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) c[k] = S(0);
+    S gu[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      gu[r] = S(0);
+#pragma unroll
+      for (int k = 0; k < M; ++k) A[r][k] = S(0);
+      if (i >= n) continue;
+      S kr[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      const S rr = a.rel[size_t(u) * n + i];
+      const S imp_i = S(a.imp[i]);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        if (k >= m) continue;
+        const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
+        if (improved) xb[size_t(i) * m + k] = X;
+        if (k < m - 1) {
+          const S gx = F::div(mul_(rr, ex[k]), imp_i);   // solver.py:86-89
+          const S W = mul_(gx, X);
+          gu[r] += W;
+          c[k] += W;
+        }
+      }
+    }
+    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+      vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
+    });
+
+    // ---------------- unrolled reverse sweep  (sinkhorn.py:278-308) ---------
+    for (int t = T; t >= 1; --t) {
+      S cv[M], vp[M], vpp[M];
+      lds_vec<S, M>(cv, vec0);
+      lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
+      if (t >= 3) lds_vec<S, M>(vpp, vh + size_t(t - 2) * P);
+#pragma unroll
+      for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        if (i >= n) continue;
+        S kr[M];
+        lds_vec<S, M>(kr, Kt + size_t(i) * P);
+        // column-softmax VJP: g_u -= sum_k S^c g_v,  gK -= S^c g_v
+        const S sig = row_dot<S, M>(kr, cv);
+        const S g = (t == T ? gu[r] : S(0)) - ut[r] * sig;
+        // row-softmax VJP with the updated g_u: gK -= S^r g_u, g_v = -sum_i S^r g_u
+        const S h = ut[r] * g;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          A[r][k] = fma(-ut[r], cv[k], A[r][k]);
+          A[r][k] = fma(-h, vp[k], A[r][k]);
+          c[k] = fma(kr[k], h, c[k]);
+        }
+        // replay u~^{t-1} from v~^{t-2}
+        if (t >= 3) {
+          ut[r] = F::rcp(row_dot<S, M>(kr, vpp));
+        } else {
+          ut[r] = S(1);
+        }
+      }
+      if (t >= 2) {
+        cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+          const S vpk = vh[size_t(t - 1) * P + k];
+          const S gv = -mul_(vpk, tot);
+          vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+        });
+      }
+    }
+
+    // ---------------- g_C = gK * (-1/eps); Adam ascent  (solver.py:105-122) -
+    const int s = a.state[ST_STEP];
+    const S bc1 = S(a.bc[2 * s]), bc2 = S(a.bc[2 * s + 1]);
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      if (i >= n) {
+#pragma unroll
+        for (int k = 0; k < M; ++k) A[r][k] = S(0);
+        continue;
+      }
+      S kr[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      const S uT = utT_s[i];
+      const S rr = a.rel[size_t(u) * n + i];
+      const S imp_i = S(a.imp[i]);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        if (k >= m) {
+          A[r][k] = S(0);
+          continue;
+        }
+        const S X = mul_(mul_(kr[k], uT), vT[k]);
+        const S W = (k < m - 1) ? mul_(F::div(mul_(rr, ex[k]), imp_i), X) : S(0);
+        const S gk = fma(kr[k], A[r][k], W);
+        const S g = mul_(gk, a.nie);
+        const size_t off = size_t(i) * m + k;
+        const S m1 = add_(mul_(a.b1, mu[off]), mul_(a.omb1, g));
+        const S v1 = add_(mul_(a.b2, vu[off]), mul_(mul_(a.omb2, g), g));
+        const S mh = F::div(m1, bc1);
+        const S vhat = F::div(v1, bc2);
+        const S c1 = add_(Cu[off], F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
+        mu[off] = m1;
+        vu[off] = v1;
+        Cu[off] = c1;
+        A[r][k] = mul_(c1, a.nie);
+      }
+    }
+  } else {
+    // INIT: initial cost C0 = -eps log(uniform) (solver.py:176-177), lvi = 0.
+    // RESUME: caller-provided C (left as is), lvi taken from the beta buffer.
+    const bool init = phase == PHASE_INIT;
+    __syncthreads();
+    if (!init && tid < m) vec2[tid] = a.beta[size_t(u) * m + tid];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        if (i < n && k < m) {
+          const size_t off = size_t(i) * m + k;
+          S c0;
+          if (init) {
+            c0 = (k == m - 1) ? a.c_dummy : a.c_real;
+            Cu[off] = c0;
+            mu[off] = S(0);
+            vu[off] = S(0);
+          } else {
+            c0 = Cu[off];
+          }
+          A[r][k] = mul_(c0, a.nie);
+        } else {
+          A[r][k] = S(0);
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ======================= forward of step k =================================
+  // inner iteration 1 in the log domain (sinkhorn.py:219-234), v^0 = lvi
+  S lv[M];
+  lds_vec<S, M>(lv, vec2);
+  S u1[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * NT;
+    u1[r] = S(0);
+    if (i >= n) continue;
+    S mx = F::ninf();
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+      if (k < m) mx = fmax(mx, add_(A[r][k], lv[k]));
+    S acc = S(0);
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+      if (k < m) acc += F::exp_(add_(A[r][k], lv[k]) - mx);
+    u1[r] = -(F::log_(acc) + mx);
+  }
+  {
+    S c[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      c[k] = F::ninf();
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (tid + r * NT < n && k < m) c[k] = fmax(c[k], add_(A[r][k], u1[r]));
+    }
+    cta_reduce_cols<S, M, NT, OpMax>(c, red, m, [&](int k, S tot) { vec1[k] = tot; });
+    S cm[M];
+    lds_vec<S, M>(cm, vec1);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      c[k] = S(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (tid + r * NT < n && k < m) c[k] += F::exp_(add_(A[r][k], u1[r]) - cm[k]);
+    }
+    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+      const S lc = (k == m - 1) ? a.log_mass_dummy : S(0);
+      const S b = lc - (F::log_(tot) + vec1[k]);
+      vec1[k] = b;
+      a.beta[size_t(u) * m + k] = b;
+      hu[k] = F::exp_(vec2[k] - b);  // v~^0
+      if (T >= 1) hu[size_t(1) * m + k] = S(1);  // v~^1
+      vec0[k] = S(1);
+    });
+  }
+  // absorb: K~ = exp(K + u^1 + v^1) = X^1
+  {
+    S bt[M];
+    lds_vec<S, M>(bt, vec1);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      const bool ok = i < n;
+      if (ok) a.alpha[size_t(u) * n + i] = u1[r];
+#pragma unroll
+      for (int k = 0; k < M; ++k) A[r][k] = (ok && k < m) ? F::exp_(add_(add_(A[r][k], u1[r]), bt[k])) : S(0);
+      ut[r] = ok ? S(1) : S(0);
+    }
+  }
+  // inner iterations 2..T, multiplicative
+  for (int t = 2; t <= T; ++t) {
+    S vv[M];
+    lds_vec<S, M>(vv, vec0);
+    S c[M];
+#pragma unroll
+    for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (tid + r * NT < n) ut[r] = F::rcp(row_dot<S, M>(A[r], vv));
+#pragma unroll
+      for (int k = 0; k < M; ++k) c[k] = fma(A[r][k], ut[r], c[k]);
+    }
+    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+      const S vn = F::div(mass(k), tot);
+      vec0[k] = vn;
+      hu[size_t(t) * m + k] = vn;
+    });
+  }
+  // per-item impact terms of this user (solver.py:206), float64
+  {
+    S vv[M];
+    lds_vec<S, M>(vv, vec0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      if (i >= n) continue;
+      const double rr = double(a.rel[size_t(u) * n + i]);
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        if (k < m - 1) {
+          const S X = mul_(mul_(A[r][k], ut[r]), vv[k]);
+          acc = fma(rr * a.expo_d[(k < m - 1) ? k : 0], double(X), acc);
+        }
+      }
+      a.partial[size_t(u) * n + i] = acc;
+    }
+  }
+}
+
+// --------------------------------------------------------------------------
+// Impact reduction over this rank's users (deterministic, fixed order):
+// split[y][i] = sum over user chunk y; the last CTA to finish sums the chunks.
+// --------------------------------------------------------------------------
+__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n, int chunks,
+                                     double* __restrict__ split, double* __restrict__ imp_local,
+                                     unsigned int* counter, const int* __restrict__ state);
+
+struct FinalizeArgs {
+  int n, world, outer_max;
+  const double* imp_all;   // [world][n]
+  const double* rel_sq;    // [n] sum_u r_ui^2 over all users
+  double exp_sq;           // sum_k e_k^2
+  double grad_threshold;
+  double* imp_cur;         // [n]
+  double* best;            // [1]
+  double* objective;       // [outer_max]
+  double* grad_norm;       // [outer_max]
+  unsigned long long* stamp;  // [outer_max+1] globaltimer ns
+  int* state;
+};
+
+__global__ void finalize_kernel(FinalizeArgs f);
+__global__ void stamp_kernel(unsigned long long* stamp);
+__global__ void flush_kernel(float* buf, size_t n);
+
+}  // namespace nsw

@@ -1,0 +1,293 @@
+"""Drop-in ``solve_fair_ranking`` backed by the sm_100a kernels.
+
+Same signature, argument meaning, return layout and exception classes as the
+reference entry point (``nswrank.solver.solve_fair_ranking``, reference
+solver.py:138-241):
+
+    policy, trace = solve_fair_ranking(relevance, exposure, shape, config)
+
+``policy`` is a ``RankingPolicy`` holding the best-objective iterate
+(solver.py:217-219, 241) as a read-only float64 [U][n][m] array; ``trace`` is a
+``SolveTrace`` with per-outer-step objective, gradient norm, Sinkhorn
+iterations and wall time (solver.py:125-135).
+
+Device-side knobs that the reference does not have live in a separate
+``DeviceOptions`` object so ``SolverConfig`` keeps the reference defaults.
+There is no CPU fallback: every call goes through libnswrank_b200.so.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import (DomainError, ExposureModel, ProblemShape, RankingPolicy, RelevanceMatrix, ShapeError,
+                   SolverConfig, SolverError, StateError)
+
+__all__ = ["DeviceOptions", "SolveTrace", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError"]
+
+NativeLibraryError = _lib.NativeLibraryError
+
+
+@dataclass
+class SolveTrace:
+    """Per-outer-iteration diagnostics (reference solver.py:125-135)."""
+
+    objective: list = field(default_factory=list)
+    grad_norm: list = field(default_factory=list)
+    sinkhorn_iterations: list = field(default_factory=list)
+    wall_time: list = field(default_factory=list)
+
+    def __len__(self) -> int:
+        return len(self.objective)
+
+
+@dataclass(frozen=True)
+class DeviceOptions:
+    """Device-only options.
+
+    dtype     "float64" (parity instantiation, default: matches the float64
+              reference) or "float32" (throughput instantiation).
+    schedule  "fixed": every Sinkhorn solve runs exactly
+              ``config.sinkhorn_max_iters`` iterations (the reference with the
+              fixed-schedule shim).
+    device    CUDA device ordinal.
+    variant   -1 = automatic tile choice; >= 0 forces a compiled tile shape.
+    use_graph capture the outer step in a CUDA graph.
+    check_every  poll the device stop flag every N outer steps.
+    """
+
+    dtype: str = "float64"
+    schedule: str = "fixed"
+    device: int = 0
+    variant: int = -1
+    use_graph: bool = True
+    check_every: int = 16
+
+    def to_c(self) -> _lib.DeviceOptionsC:
+        if self.dtype not in ("float32", "float64"):
+            raise DomainError(f"dtype must be 'float32' or 'float64', got {self.dtype!r}")
+        if self.schedule not in ("fixed", "tolerance"):
+            raise DomainError(f"schedule must be 'fixed' or 'tolerance', got {self.schedule!r}")
+        return _lib.DeviceOptionsC(
+            _lib.NSW_F64 if self.dtype == "float64" else _lib.NSW_F32,
+            _lib.NSW_SCHEDULE_FIXED if self.schedule == "fixed" else _lib.NSW_SCHEDULE_TOLERANCE,
+            int(self.device), int(self.variant), int(bool(self.use_graph)), int(self.check_every))
+
+
+def _config_c(cfg) -> _lib.SolverConfigC:
+    return _lib.SolverConfigC(float(cfg.epsilon), int(cfg.sinkhorn_max_iters), float(cfg.sinkhorn_tol),
+                              int(cfg.outer_max_iters), float(cfg.grad_threshold), float(cfg.adam_lr),
+                              float(cfg.adam_beta1), float(cfg.adam_beta2), float(cfg.adam_eps),
+                              int(bool(cfg.warm_start)))
+
+
+_ERRORS = {
+    _lib.NSW_ERR_SHAPE: ShapeError,
+    _lib.NSW_ERR_DOMAIN: DomainError,
+    _lib.NSW_ERR_STATE: StateError,
+    _lib.NSW_ERR_SOLVER: SolverError,
+    _lib.NSW_ERR_UNSUPPORTED: NotImplementedError,
+    _lib.NSW_ERR_CUDA: RuntimeError,
+    _lib.NSW_ERR_ARG: ValueError,
+}
+
+
+def check(status: int, what: str = ""):
+    if status != _lib.NSW_OK:
+        msg = _lib.last_error()
+        raise _ERRORS.get(status, RuntimeError)(f"{what}: {msg}" if what else msg)
+
+
+def _values(obj, name):
+    return np.ascontiguousarray(getattr(obj, "values", obj), dtype=np.float64)
+
+
+def _check_instance(rel: np.ndarray, expo: np.ndarray, shape) -> None:
+    """Shape checks of reference solver.py:34-43 (same messages)."""
+    U, n, m = shape.num_users, shape.num_items, shape.num_positions
+    if rel.shape != (U, n):
+        raise ShapeError(f"relevance shape {rel.shape} does not match ({U}, {n})")
+    if expo.size + 1 != m:
+        raise ShapeError(f"exposure is for m={expo.size + 1}, shape has m={m}")
+
+
+def _coerce(relevance, exposure, shape, config):
+    """Accept this package's types, the reference's own types (duck typing),
+    or plain arrays; validate like the reference's constructors."""
+    if not isinstance(relevance, RelevanceMatrix):
+        relevance = RelevanceMatrix(_values(relevance, "relevance"))
+    if not isinstance(exposure, ExposureModel):
+        exposure = ExposureModel(_values(exposure, "exposure"))
+    if not isinstance(shape, ProblemShape):
+        shape = ProblemShape(int(shape.num_users), int(shape.num_items), int(shape.num_positions))
+    if not isinstance(config, SolverConfig):
+        fields = SolverConfig.__dataclass_fields__
+        config = SolverConfig(**{k: getattr(config, k) for k in fields if hasattr(config, k)})
+    return relevance, exposure, shape, config
+
+
+class DeviceSolver:
+    """Step-level handle over one user shard (C ABI ``nsw_solver_*``).
+
+    ``relevance_local`` are this shard's rows; ``rel_sq_sum`` is sum_u r_ui^2
+    over ALL users (closed-form gradient norm); ``world`` is how many impact
+    partials the finalize step sums.
+    """
+
+    def __init__(self, relevance_local, exposure, num_items, num_positions, config, options=None,
+                 rel_sq_sum=None, world=1):
+        self.lib = _lib.load()
+        self.options = options or DeviceOptions()
+        self.config = config
+        rel = np.ascontiguousarray(relevance_local, dtype=np.float64)
+        expo = np.ascontiguousarray(exposure, dtype=np.float64)
+        self.U, self.n = rel.shape
+        self.m = int(num_positions)
+        assert self.n == num_items
+        self.T = int(config.sinkhorn_max_iters)
+        self.world = int(world)
+        rsq = None if rel_sq_sum is None else np.ascontiguousarray(rel_sq_sum, dtype=np.float64)
+        h = C.c_void_p()
+        cfg = _config_c(config)
+        opt = self.options.to_c()
+        check(self.lib.nsw_solver_create(_lib.dptr(rel), _lib.dptr(expo), self.U, self.n, self.m,
+                                         None if rsq is None else _lib.dptr(rsq), self.world,
+                                         C.byref(cfg), C.byref(opt), C.byref(h)), "nsw_solver_create")
+        self.h = h
+
+    # -- lifecycle ---------------------------------------------------------------
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.nsw_solver_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- stepping ----------------------------------------------------------------
+    def run(self, max_steps: int) -> bool:
+        done = C.c_int32(0)
+        check(self.lib.nsw_solver_run(self.h, int(max_steps), C.byref(done)), "nsw_solver_run")
+        return bool(done.value)
+
+    def local_step(self, stream: int | None = None):
+        check(self.lib.nsw_solver_local_step(self.h, C.c_void_p(stream)), "nsw_solver_local_step")
+
+    def finalize(self, stream: int | None = None):
+        check(self.lib.nsw_solver_finalize(self.h, C.c_void_p(stream)), "nsw_solver_finalize")
+
+    def exchange_buffers(self):
+        a, b = C.c_void_p(), C.c_void_p()
+        check(self.lib.nsw_solver_exchange_buffers(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+    def bind_exchange(self, local_ptr: int, gathered_ptr: int):
+        check(self.lib.nsw_solver_bind_exchange(self.h, C.c_void_p(local_ptr), C.c_void_p(gathered_ptr)))
+
+    def stream(self) -> int:
+        s = C.c_void_p()
+        check(self.lib.nsw_solver_stream(self.h, C.byref(s)))
+        return s.value or 0
+
+    def status(self):
+        p, s, e = C.c_int32(), C.c_int32(), C.c_int32()
+        check(self.lib.nsw_solver_status(self.h, C.byref(p), C.byref(s), C.byref(e)))
+        return p.value, s.value, e.value
+
+    def variant(self):
+        M, R, NT, sm = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        check(self.lib.nsw_solver_variant(self.h, C.byref(M), C.byref(R), C.byref(NT), C.byref(sm)))
+        return dict(M=M.value, R=R.value, NT=NT.value, smem=sm.value)
+
+    def launch_count(self) -> int:
+        return int(self.lib.nsw_solver_launch_count(self.h))
+
+    def time_steps(self, steps: int, flush_l2: bool = True):
+        tot, fus = C.c_float(), C.c_float()
+        check(self.lib.nsw_solver_time_steps(self.h, int(steps), int(flush_l2), C.byref(tot), C.byref(fus)))
+        return tot.value, fus.value
+
+    # -- state access ------------------------------------------------------------
+    _FIELD_SHAPES = {
+        "cost": lambda s: (s.U, s.n, s.m), "adam_m": lambda s: (s.U, s.n, s.m),
+        "adam_v": lambda s: (s.U, s.n, s.m), "xbest": lambda s: (s.U, s.n, s.m),
+        "alpha": lambda s: (s.U, s.n), "beta": lambda s: (s.U, s.m),
+        "hist": lambda s: (s.U, s.T + 1, s.m), "partial": lambda s: (s.U, s.n),
+        "imp": lambda s: (s.n,), "imp_local": lambda s: (s.n,),
+        "objective": lambda s: (s.config.outer_max_iters,), "grad_norm": lambda s: (s.config.outer_max_iters,),
+    }
+
+    def get(self, name: str) -> np.ndarray:
+        out = np.empty(self._FIELD_SHAPES[name](self), dtype=np.float64)
+        check(self.lib.nsw_solver_get(self.h, name.encode(), _lib.dptr(out), out.size), f"get {name}")
+        return out
+
+    def set(self, name: str, values) -> None:
+        arr = np.ascontiguousarray(values, dtype=np.float64).reshape(self._FIELD_SHAPES[name](self))
+        check(self.lib.nsw_solver_set(self.h, name.encode(), _lib.dptr(arr), arr.size), f"set {name}")
+
+    def set_scalar(self, name: str, value: int) -> None:
+        check(self.lib.nsw_solver_set_scalar(self.h, name.encode(), int(value)), f"set {name}")
+
+    def result(self):
+        """(best policy float64 [U][n][m], SolveTrace)."""
+        J = self.config.outer_max_iters
+        pol = np.empty((self.U, self.n, self.m), dtype=np.float64)
+        obj = np.zeros(J)
+        gn = np.zeros(J)
+        its = np.zeros(J, dtype=np.int32)
+        wall = np.zeros(J)
+        tr = _lib.TraceC(0, _lib.dptr(obj), _lib.dptr(gn), its.ctypes.data_as(C.POINTER(C.c_int32)),
+                         _lib.dptr(wall))
+        check(self.lib.nsw_solver_result(self.h, _lib.dptr(pol), C.byref(tr)), "nsw_solver_result")
+        k = tr.steps
+        trace = SolveTrace([float(x) for x in obj[:k]], [float(x) for x in gn[:k]],
+                           [int(x) for x in its[:k]], [float(x) for x in wall[:k]])
+        return pol, trace
+
+
+def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOptions | None = None):
+    """Maximise the log Nash social welfare over ranking policies on the GPU.
+
+    Drop-in for the reference ``solve_fair_ranking`` (solver.py:138-241):
+    Adam ascent on the per-user transport costs, one Sinkhorn solve per user
+    per outer step, gradients by the exact reverse mode of the unrolled
+    iterations, returning the best-objective policy and the trace.
+    """
+    relevance, exposure, shape, config = _coerce(relevance, exposure, shape, config)
+    rel = relevance.values
+    expo = exposure.values
+    _check_instance(rel, expo, shape)
+    options = options or DeviceOptions()
+    lib = _lib.load()
+    U, n, m = shape.num_users, shape.num_items, shape.num_positions
+    J = config.outer_max_iters
+    rel_c = np.ascontiguousarray(rel, dtype=np.float64)
+    expo_c = np.ascontiguousarray(expo, dtype=np.float64)
+    pol = np.empty((U, n, m), dtype=np.float64)
+    obj = np.zeros(J)
+    gn = np.zeros(J)
+    its = np.zeros(J, dtype=np.int32)
+    wall = np.zeros(J)
+    tr = _lib.TraceC(0, _lib.dptr(obj), _lib.dptr(gn), its.ctypes.data_as(C.POINTER(C.c_int32)), _lib.dptr(wall))
+    cfg = _config_c(config)
+    opt = options.to_c()
+    check(lib.nsw_solve_fair_ranking(_lib.dptr(rel_c), _lib.dptr(expo_c), U, n, m, C.byref(cfg), C.byref(opt),
+                                     _lib.dptr(pol), C.byref(tr)), "solve_fair_ranking")
+    k = tr.steps
+    trace = SolveTrace([float(x) for x in obj[:k]], [float(x) for x in gn[:k]], [int(x) for x in its[:k]],
+                       [float(x) for x in wall[:k]])
+    return RankingPolicy(pol), trace
