@@ -215,6 +215,9 @@ class OracleTrace:
     sinkhorn_iterations: list = field(default_factory=list)
     wall_time: list = field(default_factory=list)
 
+    def __len__(self) -> int:
+        return len(self.objective)
+
 
 def solve(rel, expo, p: SolverParams, dtype=np.float64, record_states=(), on_step=None):
     """Restatement of ``solve_fair_ranking`` (solver.py:138-241).

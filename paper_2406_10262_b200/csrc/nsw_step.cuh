@@ -150,8 +150,11 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
         for (int r = 0; r < R; ++r) {
           const int i = tid + r * NT;
           if (i >= n) continue;
-          const S* kr = Kt + size_t(i) * P;
-          for (int k = 0; k < m; ++k) xb[size_t(i) * m + k] = mul_(mul_(kr[k], ut[r]), vT[k]);
+          S kr[M];
+          lds_vec<S, M>(kr, Kt + size_t(i) * P);
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+            if (k < m) xb[size_t(i) * m + k] = mul_(mul_(kr[k], ut[r]), vT[k]);
         }
       }
       return;

@@ -224,7 +224,7 @@ class DeviceSolver:
     _FIELD_SHAPES = {
         "cost": lambda s: (s.U, s.n, s.m), "adam_m": lambda s: (s.U, s.n, s.m),
         "adam_v": lambda s: (s.U, s.n, s.m), "xbest": lambda s: (s.U, s.n, s.m),
-        "alpha": lambda s: (s.U, s.n), "beta": lambda s: (s.U, s.m),
+        "alpha": lambda s: (s.U, s.n), "beta": lambda s: (s.U, s.m), "lvi": lambda s: (s.U, s.m),
         "hist": lambda s: (s.U, s.T + 1, s.m), "partial": lambda s: (s.U, s.n),
         "imp": lambda s: (s.n,), "imp_local": lambda s: (s.n,),
         "objective": lambda s: (s.config.outer_max_iters,), "grad_norm": lambda s: (s.config.outer_max_iters,),

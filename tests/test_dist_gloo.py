@@ -1,0 +1,108 @@
+"""N>1 host logic on CPU: world_size-2 gloo process group.
+
+The device path shards users over ranks and exchanges the per-rank float64
+impact vectors once per outer step with an all-gather, summing them in rank
+order (paper_2406_10262_b200/distributed.py).  Here the oracle stands in for
+the per-shard device kernels and the same sharding + all-gather + combine
+logic runs over gloo; the sharded ascent must reproduce the unsharded one.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import nsw_oracle as orc
+from paper_2406_10262_b200.distributed import combine_impacts, shard_users
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _instance():
+    rng = np.random.default_rng(11)
+    rel = np.clip(rng.uniform(0.05, 1.0, (9, 14)), 1e-6, 1.0)
+    expo = 1.0 / np.log2(np.arange(2, 6))
+    return rel, expo
+
+
+def _sharded_ascent(rel_local, expo, rsq_total, eps, T, outer, exchange):
+    """Oracle arithmetic per shard; the only cross-rank step is `exchange`."""
+    U, n = rel_local.shape
+    m = expo.size + 1
+    row, col, lr, lc = orc.ranking_marginals(n, m)
+    cost = orc.initial_cost(U, n, m, eps)
+    am, av, step = np.zeros_like(cost), np.zeros_like(cost), 0
+    lvi = np.zeros((U, m))
+    gx = np.zeros_like(cost)
+    best, best_plan, objs = -np.inf, None, []
+    for it in range(outer):
+        K = cost * (-1.0 / eps)
+        fwd = orc.sinkhorn_forward(K, lr, lc, row, col, -1.0, T, lvi)
+        imp = exchange(orc.impact(rel_local, expo, fwd.plan))
+        F = float(np.log(imp).sum())
+        objs.append(F)
+        if F >= best:
+            best, best_plan = F, fwd.plan
+        if it == outer - 1:
+            break
+        orc.welfare_gradient(rel_local, expo, imp, gx)
+        g = orc.sinkhorn_backward(K, lr, lc, fwd.hist, lvi, gx, fwd.plan, fwd.log_u) * (-1.0 / eps)
+        cost, am, av, step = orc.adam_ascent(cost, g, am, av, step, 0.05, 0.9, 0.999, 1e-8)
+        lvi = fwd.log_v
+    return best_plan, objs
+
+
+def _worker(rank, world, port, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rel, expo = _instance()
+    start, stop = shard_users(rel.shape[0], world, rank)
+    rsq = torch.tensor((rel[start:stop] ** 2).sum(0))
+    dist.all_reduce(rsq)
+    n = rel.shape[1]
+
+    def exchange(local):
+        gathered = torch.zeros(world * n, dtype=torch.float64)
+        dist.all_gather_into_tensor(gathered, torch.tensor(local, dtype=torch.float64))
+        return combine_impacts(gathered.numpy().reshape(world, n))
+
+    plan, objs = _sharded_ascent(rel[start:stop], expo, rsq.numpy(), 0.2, 12, 8, exchange)
+    np.savez(os.path.join(outdir, f"rank{rank}.npz"), plan=plan, objs=np.array(objs), start=start, stop=stop,
+             rsq=rsq.numpy())
+    dist.destroy_process_group()
+
+
+def test_shard_users_partition():
+    for U in (1, 7, 100, 1001):
+        for world in (1, 2, 3, 8):
+            if world > U:
+                continue
+            blocks = [shard_users(U, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == U
+            assert all(blocks[i][1] == blocks[i + 1][0] for i in range(world - 1))
+            sizes = [b - a for a, b in blocks]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_two_rank_gloo_sharded_ascent_matches_unsharded(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    rel, expo = _instance()
+    parts = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    # every rank saw the same objective trace (identical exchange result)
+    assert np.array_equal(parts[0]["objs"], parts[1]["objs"])
+    np.testing.assert_allclose(parts[0]["rsq"], (rel ** 2).sum(0), rtol=1e-15)
+    plan = np.concatenate([p["plan"] for p in parts], axis=0)
+    p = orc.SolverParams(epsilon=0.2, sinkhorn_max_iters=12, outer_max_iters=8, grad_threshold=1e-300)
+    x, tr, _ = orc.solve(rel, expo, p)
+    assert np.abs(plan - x).max() < 1e-10
+    assert np.abs(parts[0]["objs"] / np.array(tr.objective) - 1).max() < 1e-13
