@@ -182,9 +182,8 @@ nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
   void* args64[] = {&s->a64};
   CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
                             s->smem, st));
-  const int bx = (s->n + 127) / 128;
-  impact_reduce_kernel<<<dim3(bx, s->chunks), 128, 0, st>>>(s->partial, s->U, s->n, s->chunks, s->split,
-                                                            s->imp_local, s->counter, s->state);
+  impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n,
+                                                                                  s->imp_local, s->state);
   CUDA_TRY(cudaGetLastError());
   s->launches += 2;
   return NSW_OK;
@@ -274,11 +273,6 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   if (s->opt.check_every <= 0) s->opt.check_every = 8;
   s->var = var;
   s->smem = var->smem(T);
-  {
-    // user chunks of the impact reduction: ~2 CTAs per SM in total
-    const int bx = (n + 127) / 128;
-    s->chunks = std::max(1, std::min(users_local, (2 * 148 + bx - 1) / bx));
-  }
   const size_t es = sizeof_dtype(s->dtype);
   const size_t cells = size_t(users_local) * n * m;
   nsw_status e = NSW_OK;
@@ -301,7 +295,6 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->expo, size_t(m) * es);
   ALLOC(s->expo_d, size_t(m) * 8);
   ALLOC(s->partial, size_t(users_local) * n * 8);
-  ALLOC(s->split, size_t(s->chunks) * n * 8);
   ALLOC(s->own_imp_local, size_t(n) * 8);
   ALLOC(s->own_imp_all, size_t(world) * n * 8);
   ALLOC(s->imp_cur, size_t(n) * 8);
@@ -624,10 +617,8 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
     CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT),
                               s->dtype == NSW_F64 ? args64 : args32, s->smem, s->stream));
     CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
-    const int bx = (s->n + 127) / 128;
-    impact_reduce_kernel<<<dim3(bx, s->chunks), 128, 0, s->stream>>>(s->partial, s->U, s->n, s->chunks,
-                                                                       s->split, s->imp_local, s->counter,
-                                                                       s->state);
+    impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, s->stream>>>(
+        s->partial, s->U, s->n, s->imp_local, s->state);
     finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));

@@ -6,34 +6,37 @@
 
 namespace nsw {
 
-__global__ void __launch_bounds__(128) impact_reduce_kernel(const double* __restrict__ partial, int U, int n,
-                                                            int chunks, double* __restrict__ split,
-                                                            double* __restrict__ imp_local,
-                                                            unsigned int* counter,
-                                                            const int* __restrict__ state) {
+// One CTA per IMP_ITEMS consecutive items; its 256 threads stride over the
+// users (thread t: item t % IMP_ITEMS, user lane t / IMP_ITEMS), then a fixed
+// shared-memory tree combines the lanes: one pass, deterministic order.
+__global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double* __restrict__ partial, int U,
+                                                                    int n, double* __restrict__ imp_local,
+                                                                    const int* __restrict__ state) {
   const int phase = state[ST_PHASE];
   if (phase != PHASE_INIT && phase != PHASE_RUNNING && phase != PHASE_RESUME) return;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int y = blockIdx.y;
-  const int u0 = int((long long)y * U / chunks), u1 = int((long long)(y + 1) * U / chunks);
+  constexpr int LANES = IMP_THREADS / IMP_ITEMS;
+  __shared__ double red[IMP_THREADS];
+  const int j = threadIdx.x % IMP_ITEMS;
+  const int l = threadIdx.x / IMP_ITEMS;
+  const int i = blockIdx.x * IMP_ITEMS + j;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (i < n) {
-    double acc = 0.0;
-    for (int u = u0; u < u1; ++u) acc += partial[size_t(u) * n + i];
-    split[size_t(y) * n + i] = acc;
+    int u = l;
+    for (; u + 3 * LANES < U; u += 4 * LANES) {
+      a0 += partial[size_t(u) * n + i];
+      a1 += partial[size_t(u + LANES) * n + i];
+      a2 += partial[size_t(u + 2 * LANES) * n + i];
+      a3 += partial[size_t(u + 3 * LANES) * n + i];
+    }
+    for (; u < U; u += LANES) a0 += partial[size_t(u) * n + i];
   }
-  __threadfence();
+  red[threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int j = threadIdx.x; j < n; j += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < chunks; ++c) acc += __ldcg(split + size_t(c) * n + j);
-    imp_local[j] = acc;
+  for (int w = LANES / 2; w > 0; w >>= 1) {
+    if (l < w) red[threadIdx.x] += red[threadIdx.x + w * IMP_ITEMS];
+    __syncthreads();
   }
-  if (threadIdx.x == 0) *counter = 0u;
+  if (l == 0 && i < n) imp_local[i] = red[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {

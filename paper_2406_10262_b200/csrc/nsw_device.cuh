@@ -38,6 +38,12 @@ struct Fp<float> {
   static __device__ __forceinline__ float exp_(float x) { return expf(x); }
   static __device__ __forceinline__ float log_(float x) { return logf(x); }
   static __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+  // hot-loop reciprocal: one MUFU.RCP (<= 1 ulp), no IEEE fix-up branch
+  static __device__ __forceinline__ float rcp_fast(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
   static __device__ __forceinline__ float sqrt_(float x) { return __fsqrt_rn(x); }
   static __device__ __forceinline__ float ninf() { return -CUDART_INF_F; }
@@ -49,6 +55,7 @@ struct Fp<double> {
   static __device__ __forceinline__ double exp_(double x) { return exp(x); }
   static __device__ __forceinline__ double log_(double x) { return log(x); }
   static __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
+  static __device__ __forceinline__ double rcp_fast(double x) { return __drcp_rn(x); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
   static __device__ __forceinline__ double sqrt_(double x) { return __dsqrt_rn(x); }
   static __device__ __forceinline__ double ninf() { return -CUDART_INF; }

@@ -1,6 +1,7 @@
 // One translation unit per (scalar type, M): compiled with
 //   -DNSW_F64=0|1 -DNSW_M=<columns>
-// and registers the (rows/thread, threads/CTA) tile shapes for that pair.
+// and registers the (rows/thread, threads/CTA, min CTAs/SM) tile shapes for
+// that pair.  MINB caps registers at 64K / (NT * MINB) per thread.
 #include "nsw_registry.h"
 #include "nsw_step.cuh"
 
@@ -25,45 +26,53 @@ size_t smem_of(int T) {
 
 #define NSW_CAT2(a, b) a##b
 #define NSW_CAT(a, b) NSW_CAT2(a, b)
-#define NSW_REG(R, NT)                                                                        \
-  Registrar NSW_CAT(reg_, __LINE__)(Variant{NSW_DT, NSW_M, R, NT,                             \
-                                            (const void*)&step_kernel<NSW_S, NSW_M, R, NT>, \
+#define NSW_REG(R, NT, MINB)                                                                        \
+  Registrar NSW_CAT(reg_, __LINE__)(Variant{NSW_DT, NSW_M, R, NT,                                   \
+                                            (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB>, \
                                             &smem_of<R, NT>});
 
 #if NSW_F64
 #if NSW_M <= 16
-NSW_REG(1, 64)
-NSW_REG(1, 128)
-NSW_REG(1, 256)
-NSW_REG(2, 256)
-NSW_REG(2, 512)
+NSW_REG(1, 64, 1)
+NSW_REG(1, 128, 1)
+NSW_REG(1, 256, 1)
+NSW_REG(2, 256, 1)
+NSW_REG(2, 512, 1)
 #else
-NSW_REG(1, 64)
-NSW_REG(1, 128)
-NSW_REG(1, 256)
-NSW_REG(1, 512)
+NSW_REG(1, 64, 1)
+NSW_REG(1, 128, 1)
+NSW_REG(1, 256, 1)
+NSW_REG(1, 512, 1)
 #endif
 #else
-#if NSW_M <= 16
-NSW_REG(1, 64)
-NSW_REG(2, 64)
-NSW_REG(4, 64)
-NSW_REG(8, 64)
-NSW_REG(4, 128)
-NSW_REG(8, 128)
-NSW_REG(8, 256)
+#if NSW_M <= 11
+NSW_REG(1, 64, 1)
+NSW_REG(2, 64, 1)
+NSW_REG(4, 64, 6)
+NSW_REG(8, 64, 6)
+NSW_REG(4, 128, 3)
+NSW_REG(8, 128, 3)
+NSW_REG(8, 256, 1)
+#elif NSW_M <= 16
+NSW_REG(1, 64, 1)
+NSW_REG(2, 64, 1)
+NSW_REG(4, 64, 4)
+NSW_REG(8, 64, 4)
+NSW_REG(4, 128, 2)
+NSW_REG(8, 128, 2)
+NSW_REG(8, 256, 1)
 #elif NSW_M <= 24
-NSW_REG(1, 64)
-NSW_REG(2, 64)
-NSW_REG(4, 64)
-NSW_REG(4, 128)
-NSW_REG(4, 256)
+NSW_REG(1, 64, 1)
+NSW_REG(2, 64, 1)
+NSW_REG(4, 64, 4)
+NSW_REG(4, 128, 1)
+NSW_REG(4, 256, 1)
 #else
-NSW_REG(1, 64)
-NSW_REG(2, 64)
-NSW_REG(2, 128)
-NSW_REG(2, 256)
-NSW_REG(2, 512)
+NSW_REG(1, 64, 1)
+NSW_REG(2, 64, 1)
+NSW_REG(2, 128, 1)
+NSW_REG(2, 256, 1)
+NSW_REG(2, 512, 1)
 #endif
 #endif
 

@@ -52,43 +52,49 @@ __device__ __forceinline__ float add_(float a, float b) { return __fadd_rn(a, b)
 template <>
 __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a, b); }
 
+// Row dot product with two interleaved accumulators (halves the dependent
+// FMA chain).  Every place that forms u~ = 1/(K~ v~) uses this one function,
+// so the forward and the backward's replay produce bit-identical u~.
 template <typename S, int M>
-__device__ __forceinline__ S row_dot(const S (&x)[M], const S (&y)[M]) {
-  S s = S(0);
+__device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
+  S s0 = S(0), s1 = S(0);
 #pragma unroll
-  for (int k = 0; k < M; ++k) s = fma(x[k], y[k], s);
-  return s;
-}
-
-template <typename S, int M>
-__device__ __forceinline__ S row_dot2(const S* x, const S (&y)[M]) {
-  S s = S(0);
-#pragma unroll
-  for (int k = 0; k < M; ++k) s = fma(x[k], y[k], s);
-  return s;
+  for (int k = 0; k + 1 < M; k += 2) {
+    s0 = fma(x[k], y[k], s0);
+    s1 = fma(x[k + 1], y[k + 1], s1);
+  }
+  if constexpr (M % 2) s0 = fma(x[M - 1], y[M - 1], s0);
+  return s0 + s1;
 }
 
 template <typename S, int M, int R, int NT>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
-  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + size_t(NT) * R);
+  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + 2 * size_t(NT) * R);
 }
 
-template <typename S, int M, int R, int NT>
-__global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
+// Structure: the per-step phases that touch every cell once (K~ rebuild,
+// seed, Adam, log-domain iteration 1) run as runtime loops over this
+// thread's rows through the shared-memory tile Kt, so they add no register
+// pressure; only the two hot loops (forward iterations 2..T and the T
+// reverse levels) hold the R x M tile in registers.
+template <typename S, int M, int R, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   using F = Fp<S>;
   constexpr int P = Pitch<S, M>::value;
   constexpr int NW = NT / 32;
-  static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
+  constexpr int PAIR = R >= 2 ? 2 : 1;
+  static_assert(NT % 32 == 0 && M <= NT && P <= NT && R % PAIR == 0, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
-  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K~ rows (backward)
+  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K / K~ / gK rows
   S* vh = Kt + size_t(NT) * R * P;          // [T+1][P]   v~ history
   S* red = vh + size_t(T + 1) * P;          // [NW][P]    column partials
   S* vec0 = red + NW * P;                   // [P] scaling vector / cv
   S* vec1 = vec0 + P;                       // [P] beta / column max
   S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
-  S* utT_s = vec2 + P;                      // [NT*R] u~^T per row
+  S* rowA = vec2 + P;                       // [NT*R] u~^T per row, then u^1
+  S* rowB = rowA + size_t(NT) * R;          // [NT*R] seed g_u per row
 
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) return;
@@ -102,7 +108,8 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
   S* vu = a.av + ubase;
   S* xb = a.xbest + ubase;
   S* hu = a.hist + size_t(u) * (T + 1) * m;
-
+  const S* relu = a.rel + size_t(u) * n;
+  auto ok = [&](int r) { return tid + r * NT < n; };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
   auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
 
@@ -111,9 +118,9 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
     vec1[tid] = S(0);
     vec2[tid] = S(0);
   }
-
-  S A[R][M];  // forward: K~ ; backward: adjoint G  (gK = W + K~ .* G)
-  S ut[R];    // current u~ per row
+  S ex[M];
+#pragma unroll
+  for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
 
   if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
     // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
@@ -124,116 +131,150 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
       vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
     }
     __syncthreads();
-    S bt[M], vT1[M], vT[M];
-    lds_vec<S, M>(bt, vec1);
+    S vT[M];
     lds_vec<S, M>(vT, vh + size_t(T) * P);
-    if (T >= 2) lds_vec<S, M>(vT1, vh + size_t(T - 1) * P);
+    {
+      S bt[M], vT1[M];
+      lds_vec<S, M>(bt, vec1);
+      lds_vec<S, M>(vT1, vh + size_t(T >= 2 ? T - 1 : 0) * P);
+#pragma unroll 1
+      for (int i = tid; i < NT * R; i += NT) {
+        const bool v = i < n;
+        S kr[M];
+        const S al = v ? a.alpha[size_t(u) * n + i] : S(0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
-      S kr[M];
-      const S al = i < n ? a.alpha[size_t(u) * n + i] : S(0);
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        kr[k] = (i < n && k < m) ? F::exp_(add_(add_(mul_(Cu[size_t(i) * m + k], a.nie), al), bt[k])) : S(0);
-      sts_vec<S, M>(Kt + size_t(i) * P, kr);
-      S uT = S(0);
-      if (i < n) uT = (T >= 2) ? F::rcp(row_dot<S, M>(kr, vT1)) : S(1);
-      utT_s[i] = uT;
-      ut[r] = uT;
+        for (int k = 0; k < M; ++k)
+          kr[k] = (v && k < m) ? F::exp_(add_(add_(mul_(Cu[size_t(i) * m + k], a.nie), al), bt[k])) : S(0);
+        sts_vec<S, M>(Kt + size_t(i) * P, kr);
+        rowA[i] = v ? ((T >= 2) ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(1)) : S(0);
+      }
     }
     const int improved = a.state[ST_IMPROVED];
     if (phase == PHASE_DONE_PENDING) {
       // the stop fired after step k-1's forward: only its policy is still owed
       if (improved) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int i = tid + r * NT;
-          if (i >= n) continue;
+#pragma unroll 1
+        for (int i = tid; i < n; i += NT) {
           S kr[M];
           lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          const S uT = rowA[i];
 #pragma unroll
           for (int k = 0; k < M; ++k)
-            if (k < m) xb[size_t(i) * m + k] = mul_(mul_(kr[k], ut[r]), vT[k]);
+            if (k < m) xb[size_t(i) * m + k] = mul_(mul_(kr[k], uT), vT[k]);
         }
       }
       return;
     }
 
     // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
-    S ex[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
-    S c[M];
-#pragma unroll
-    for (int k = 0; k < M; ++k) c[k] = S(0);
-    S gu[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
-      gu[r] = S(0);
-#pragma unroll
-      for (int k = 0; k < M; ++k) A[r][k] = S(0);
-      if (i >= n) continue;
-      S kr[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S rr = a.rel[size_t(u) * n + i];
-      const S imp_i = S(a.imp[i]);
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        if (k >= m) continue;
-        const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
-        if (improved) xb[size_t(i) * m + k] = X;
-        if (k < m - 1) {
-          const S gx = F::div(mul_(rr, ex[k]), imp_i);   // solver.py:86-89
-          const S W = mul_(gx, X);
-          gu[r] += W;
-          c[k] += W;
-        }
-      }
-    }
-    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-      vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
-    });
-
-    // ---------------- unrolled reverse sweep  (sinkhorn.py:278-308) ---------
-    for (int t = T; t >= 1; --t) {
-      S cv[M], vp[M], vpp[M];
-      lds_vec<S, M>(cv, vec0);
-      lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
-      if (t >= 3) lds_vec<S, M>(vpp, vh + size_t(t - 2) * P);
+    {
+      S c[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll 1
+      for (int i = tid; i < NT * R; i += NT) {
+        const bool v = i < n;
+        S kr[M];
+        lds_vec<S, M>(kr, Kt + size_t(i) * P);
+        const S uT = rowA[i];
+        const S rr = v ? relu[i] : S(0);
+        const S imp_i = v ? S(a.imp[i]) : S(1);
+        S gsum = S(0);
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          if (k >= m) continue;
+          const S X = mul_(mul_(kr[k], uT), vT[k]);
+          if (improved && v) xb[size_t(i) * m + k] = X;
+          if (k < m - 1) {
+            const S W = mul_(F::div(mul_(rr, ex[k]), imp_i), X);   // gx = r e / Imp, solver.py:86-89
+            gsum += W;
+            c[k] += W;
+          }
+        }
+        rowB[i] = gsum;
+      }
+      cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+        vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
+      });
+    }
+
+    // ---------------- unrolled reverse sweep  (sinkhorn.py:278-308) ---------
+    // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
+    //   g_u  <- [t==T] g_u^seed - u~ (K~ cv)_i                  column VJP
+    //   h    <- u~ g_u
+    //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
+    //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
+    //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 3)
+    {
+      S A[R][M];  // adjoint G: gK = W + K~ .* G
+      S ut[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        ut[r] = rowA[tid + r * NT];
+#pragma unroll
+        for (int k = 0; k < M; ++k) A[r][k] = S(0);
+      }
+      for (int t = T; t >= 1; --t) {
+        S cv[M], vp[M], vpp[M], c[M];
+        lds_vec<S, M>(cv, vec0);
+        lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
+        lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
+        const bool first = t == T;
+        const bool replay = t >= 3;
+#pragma unroll
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+        for (int r = 0; r < R; r += PAIR) {
+          S kr[PAIR][M], h[PAIR];
+#pragma unroll
+          for (int q = 0; q < PAIR; ++q) lds_vec<S, M>(kr[q], Kt + size_t(tid + (r + q) * NT) * P);
+#pragma unroll
+          for (int q = 0; q < PAIR; ++q) {
+            const S sig = rdot<S, M>(kr[q], cv);
+            const S gs = first ? rowB[tid + (r + q) * NT] : S(0);
+            h[q] = ut[r + q] * (gs - ut[r + q] * sig);
+          }
+#pragma unroll
+          for (int q = 0; q < PAIR; ++q)
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+              A[r + q][k] = fma(-ut[r + q], cv[k], A[r + q][k]);
+              A[r + q][k] = fma(-h[q], vp[k], A[r + q][k]);
+            }
+#pragma unroll
+          for (int k = 0; k < M; ++k)
+#pragma unroll
+            for (int q = 0; q < PAIR; ++q) c[k] = fma(kr[q][k], h[q], c[k]);
+#pragma unroll
+          for (int q = 0; q < PAIR; ++q) {
+            const S rp = F::rcp_fast(rdot<S, M>(kr[q], vpp));
+            ut[r + q] = ok(r + q) ? (replay ? rp : S(1)) : S(0);
+          }
+        }
+        if (t >= 2) {
+          cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+            const S vpk = vh[size_t(t - 1) * P + k];
+            const S gv = -mul_(vpk, tot);
+            vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+          });
+        }
+      }
+      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
-        if (i >= n) continue;
-        S kr[M];
+        S kr[M], gk[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        // column-softmax VJP: g_u -= sum_k S^c g_v,  gK -= S^c g_v
-        const S sig = row_dot<S, M>(kr, cv);
-        const S g = (t == T ? gu[r] : S(0)) - ut[r] * sig;
-        // row-softmax VJP with the updated g_u: gK -= S^r g_u, g_v = -sum_i S^r g_u
-        const S h = ut[r] * g;
+        const S uT = rowA[i];
+        const S rr = ok(r) ? relu[i] : S(0);
+        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          A[r][k] = fma(-ut[r], cv[k], A[r][k]);
-          A[r][k] = fma(-h, vp[k], A[r][k]);
-          c[k] = fma(kr[k], h, c[k]);
+          const S X = mul_(mul_(kr[k], uT), vT[k]);
+          const S W = (k < m - 1) ? mul_(F::div(mul_(rr, ex[k]), imp_i), X) : S(0);
+          gk[k] = fma(kr[k], A[r][k], W);
         }
-        // replay u~^{t-1} from v~^{t-2}
-        if (t >= 3) {
-          ut[r] = F::rcp(row_dot<S, M>(kr, vpp));
-        } else {
-          ut[r] = S(1);
-        }
-      }
-      if (t >= 2) {
-        cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-          const S vpk = vh[size_t(t - 1) * P + k];
-          const S gv = -mul_(vpk, tot);
-          vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
-        });
+        sts_vec<S, M>(Kt + size_t(i) * P, gk);
       }
     }
 
@@ -241,40 +282,28 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
     const int s = a.state[ST_STEP];
     const S bc1 = S(a.bc[2 * s]), bc2 = S(a.bc[2 * s + 1]);
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
-      if (i >= n) {
-#pragma unroll
-        for (int k = 0; k < M; ++k) A[r][k] = S(0);
-        continue;
-      }
-      S kr[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S uT = utT_s[i];
-      const S rr = a.rel[size_t(u) * n + i];
-      const S imp_i = S(a.imp[i]);
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) {
+      S gk[M], kn[M];
+      lds_vec<S, M>(gk, Kt + size_t(i) * P);
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        if (k >= m) {
-          A[r][k] = S(0);
-          continue;
+        kn[k] = S(0);
+        if (k < m) {
+          const S g = mul_(gk[k], a.nie);
+          const size_t off = size_t(i) * m + k;
+          const S m1 = add_(mul_(a.b1, mu[off]), mul_(a.omb1, g));
+          const S v1 = add_(mul_(a.b2, vu[off]), mul_(mul_(a.omb2, g), g));
+          const S mh = F::div(m1, bc1);
+          const S vhat = F::div(v1, bc2);
+          const S c1 = add_(Cu[off], F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
+          mu[off] = m1;
+          vu[off] = v1;
+          Cu[off] = c1;
+          kn[k] = mul_(c1, a.nie);
         }
-        const S X = mul_(mul_(kr[k], uT), vT[k]);
-        const S W = (k < m - 1) ? mul_(F::div(mul_(rr, ex[k]), imp_i), X) : S(0);
-        const S gk = fma(kr[k], A[r][k], W);
-        const S g = mul_(gk, a.nie);
-        const size_t off = size_t(i) * m + k;
-        const S m1 = add_(mul_(a.b1, mu[off]), mul_(a.omb1, g));
-        const S v1 = add_(mul_(a.b2, vu[off]), mul_(mul_(a.omb2, g), g));
-        const S mh = F::div(m1, bc1);
-        const S vhat = F::div(v1, bc2);
-        const S c1 = add_(Cu[off], F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
-        mu[off] = m1;
-        vu[off] = v1;
-        Cu[off] = c1;
-        A[r][k] = mul_(c1, a.nie);
       }
+      sts_vec<S, M>(Kt + size_t(i) * P, kn);
     }
   } else {
     // INIT: initial cost C0 = -eps log(uniform) (solver.py:176-177), lvi = 0.
@@ -282,12 +311,13 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
     const bool init = phase == PHASE_INIT;
     __syncthreads();
     if (!init && tid < m) vec2[tid] = a.beta[size_t(u) * m + tid];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) {
+      S kn[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) {
-        if (i < n && k < m) {
+        kn[k] = S(0);
+        if (k < m) {
           const size_t off = size_t(i) * m + k;
           S c0;
           if (init) {
@@ -298,53 +328,53 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
           } else {
             c0 = Cu[off];
           }
-          A[r][k] = mul_(c0, a.nie);
-        } else {
-          A[r][k] = S(0);
+          kn[k] = mul_(c0, a.nie);
         }
       }
+      sts_vec<S, M>(Kt + size_t(i) * P, kn);
     }
   }
   __syncthreads();
 
   // ======================= forward of step k =================================
-  // inner iteration 1 in the log domain (sinkhorn.py:219-234), v^0 = lvi
-  S lv[M];
-  lds_vec<S, M>(lv, vec2);
-  S u1[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = tid + r * NT;
-    u1[r] = S(0);
-    if (i >= n) continue;
-    S mx = F::ninf();
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-      if (k < m) mx = fmax(mx, add_(A[r][k], lv[k]));
-    S acc = S(0);
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-      if (k < m) acc += F::exp_(add_(A[r][k], lv[k]) - mx);
-    u1[r] = -(F::log_(acc) + mx);
-  }
+  // inner iteration 1 in the log domain (sinkhorn.py:219-234), v^0 = lvi;
+  // K = C * (-1/eps) is in the tile rows i < n.
   {
-    S c[M];
+    S lv[M], c[M];
+    lds_vec<S, M>(lv, vec2);
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      c[k] = F::ninf();
+    for (int k = 0; k < M; ++k) c[k] = F::ninf();
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) {
+      S kr[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      S mx = F::ninf();
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (tid + r * NT < n && k < m) c[k] = fmax(c[k], add_(A[r][k], u1[r]));
+      for (int k = 0; k < M; ++k)
+        if (k < m) mx = fmax(mx, add_(kr[k], lv[k]));
+      S acc = S(0);
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k < m) acc += F::exp_(add_(kr[k], lv[k]) - mx);
+      const S u1 = -(F::log_(acc) + mx);
+      rowA[i] = u1;
+#pragma unroll
+      for (int k = 0; k < M; ++k)
+        if (k < m) c[k] = fmax(c[k], add_(kr[k], u1));
     }
     cta_reduce_cols<S, M, NT, OpMax>(c, red, m, [&](int k, S tot) { vec1[k] = tot; });
     S cm[M];
     lds_vec<S, M>(cm, vec1);
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      c[k] = S(0);
+    for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll 1
+    for (int i = tid; i < n; i += NT) {
+      S kr[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      const S u1 = rowA[i];
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (tid + r * NT < n && k < m) c[k] += F::exp_(add_(A[r][k], u1[r]) - cm[k]);
+      for (int k = 0; k < M; ++k)
+        if (k < m) c[k] += F::exp_(add_(kr[k], u1) - cm[k]);
     }
     cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
       const S lc = (k == m - 1) ? a.log_mass_dummy : S(0);
@@ -355,33 +385,42 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
       if (T >= 1) hu[size_t(1) * m + k] = S(1);  // v~^1
       vec0[k] = S(1);
     });
-  }
-  // absorb: K~ = exp(K + u^1 + v^1) = X^1
-  {
+    // absorb: K~ = exp(K + u^1 + v^1) = X^1 (rows >= n stay zero)
     S bt[M];
     lds_vec<S, M>(bt, vec1);
+#pragma unroll 1
+    for (int i = tid; i < NT * R; i += NT) {
+      const bool v = i < n;
+      S kr[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      const S u1 = v ? rowA[i] : S(0);
+      if (v) a.alpha[size_t(u) * n + i] = u1;
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
-      const bool ok = i < n;
-      if (ok) a.alpha[size_t(u) * n + i] = u1[r];
-#pragma unroll
-      for (int k = 0; k < M; ++k) A[r][k] = (ok && k < m) ? F::exp_(add_(add_(A[r][k], u1[r]), bt[k])) : S(0);
-      ut[r] = ok ? S(1) : S(0);
+      for (int k = 0; k < M; ++k) kr[k] = (v && k < m) ? F::exp_(add_(add_(kr[k], u1), bt[k])) : S(0);
+      sts_vec<S, M>(Kt + size_t(i) * P, kr);
     }
   }
-  // inner iterations 2..T, multiplicative
-  for (int t = 2; t <= T; ++t) {
-    S vv[M];
-    lds_vec<S, M>(vv, vec0);
-    S c[M];
+  // inner iterations 2..T, multiplicative: u~ = 1/(K~ v~), v~ = colmass/(K~' u~)
+  S A[R][M];  // K~, register resident
+  S ut[R];
 #pragma unroll
-    for (int k = 0; k < M; ++k) c[k] = S(0);
+  for (int r = 0; r < R; ++r) {
+    lds_vec<S, M>(A[r], Kt + size_t(tid + r * NT) * P);
+    ut[r] = ok(r) ? S(1) : S(0);
+  }
+  for (int t = 2; t <= T; ++t) {
+    S vv[M], c[M];
+    lds_vec<S, M>(vv, vec0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      if (tid + r * NT < n) ut[r] = F::rcp(row_dot<S, M>(A[r], vv));
+      const S rp = F::rcp_fast(rdot<S, M>(A[r], vv));
+      ut[r] = ok(r) ? rp : S(0);
+    }
 #pragma unroll
-      for (int k = 0; k < M; ++k) c[k] = fma(A[r][k], ut[r], c[k]);
+    for (int k = 0; k < M; ++k) {
+      c[k] = A[0][k] * ut[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) c[k] = fma(A[r][k], ut[r], c[k]);
     }
     cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
       const S vn = F::div(mass(k), tot);
@@ -396,8 +435,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = tid + r * NT;
-      if (i >= n) continue;
-      const double rr = double(a.rel[size_t(u) * n + i]);
+      const double rr = ok(r) ? double(relu[i]) : 0.0;
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
@@ -406,7 +444,7 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
           acc = fma(rr * a.expo_d[(k < m - 1) ? k : 0], double(X), acc);
         }
       }
-      a.partial[size_t(u) * n + i] = acc;
+      if (ok(r)) a.partial[size_t(u) * n + i] = acc;
     }
   }
 }
@@ -415,9 +453,10 @@ __global__ void __launch_bounds__(NT) step_kernel(const StepArgs<S> a) {
 // Impact reduction over this rank's users (deterministic, fixed order):
 // split[y][i] = sum over user chunk y; the last CTA to finish sums the chunks.
 // --------------------------------------------------------------------------
-__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n, int chunks,
-                                     double* __restrict__ split, double* __restrict__ imp_local,
-                                     unsigned int* counter, const int* __restrict__ state);
+constexpr int IMP_THREADS = 256;
+constexpr int IMP_ITEMS = 8;
+__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n,
+                                     double* __restrict__ imp_local, const int* __restrict__ state);
 
 struct FinalizeArgs {
   int n, world, outer_max;
