@@ -16,7 +16,7 @@
 
 #include "../../include/nswrank_b200.h"
 #include "nsw_registry.h"
-#include "nsw_step.cuh"
+#include "nsw_step_kernel.cuh"
 
 namespace nsw {
 std::vector<Variant>& variant_registry() {

@@ -2,7 +2,7 @@
 // and the scalar epilogue (objective, gradient norm, best iterate, stopping
 // rule; solver.py:207-223).  Both are latency kernels; they are ordered on
 // the solver's stream right after the fused per-user step kernel.
-#include "nsw_step.cuh"
+#include "nsw_step_kernel.cuh"
 
 namespace nsw {
 

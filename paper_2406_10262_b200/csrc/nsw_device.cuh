@@ -21,6 +21,8 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace nsw {
 
 // PHASE_RESUME: forward of step k from a caller-provided cost tensor, with the
@@ -45,6 +47,7 @@ struct Fp<float> {
     return y;
   }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }
+  static __device__ __forceinline__ float div_fast(float a, float b) { return a * rcp_fast(b); }
   static __device__ __forceinline__ float sqrt_(float x) { return __fsqrt_rn(x); }
   static __device__ __forceinline__ float ninf() { return -CUDART_INF_F; }
   static constexpr int kVec = 4;  // elements per 16-byte vector
@@ -57,6 +60,7 @@ struct Fp<double> {
   static __device__ __forceinline__ double rcp(double x) { return __drcp_rn(x); }
   static __device__ __forceinline__ double rcp_fast(double x) { return __drcp_rn(x); }
   static __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, b); }
+  static __device__ __forceinline__ double div_fast(double a, double b) { return __ddiv_rn(a, b); }
   static __device__ __forceinline__ double sqrt_(double x) { return __dsqrt_rn(x); }
   static __device__ __forceinline__ double ninf() { return -CUDART_INF; }
   static constexpr int kVec = 2;

@@ -3,7 +3,7 @@
 // and registers the (rows/thread, threads/CTA, min CTAs/SM) tile shapes for
 // that pair.  MINB caps registers at 64K / (NT * MINB) per thread.
 #include "nsw_registry.h"
-#include "nsw_step.cuh"
+#include "nsw_step_kernel.cuh"
 
 #ifndef NSW_M
 #error "NSW_M must be defined"

@@ -67,22 +67,31 @@ __device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
   return s0 + s1;
 }
 
+// 16-byte vector of scalars (float4 / double2) for coalesced tile traffic.
+template <typename S>
+union V16 {
+  typename std::conditional<sizeof(S) == 4, float4, double2>::type v;
+  S s[16 / sizeof(S)];
+};
+
 template <typename S, int M, int R, int NT>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + 2 * size_t(NT) * R);
 }
 
-// Structure: the per-step phases that touch every cell once (K~ rebuild,
-// seed, Adam, log-domain iteration 1) run as runtime loops over this
-// thread's rows through the shared-memory tile Kt, so they add no register
-// pressure; only the two hot loops (forward iterations 2..T and the T
+// Structure: the per-step phases that touch every cell once move the user's
+// contiguous [n][m] tiles between HBM and the shared-memory tile Kt with
+// coalesced 16-byte accesses (element-wise phases: K~ rebuild, Adam, the
+// policy write) or as runtime loops over this thread's rows (seed, log-domain
+// iteration 1); only the two hot loops (forward iterations 2..T and the T
 // reverse levels) hold the R x M tile in registers.
 template <typename S, int M, int R, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   using F = Fp<S>;
   constexpr int P = Pitch<S, M>::value;
   constexpr int NW = NT / 32;
+  constexpr int V = 16 / sizeof(S);
   constexpr int PAIR = R >= 2 ? 2 : 1;
   static_assert(NT % 32 == 0 && M <= NT && P <= NT && R % PAIR == 0, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -93,7 +102,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* vec0 = red + NW * P;                   // [P] scaling vector / cv
   S* vec1 = vec0 + P;                       // [P] beta / column max
   S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
-  S* rowA = vec2 + P;                       // [NT*R] u~^T per row, then u^1
+  S* rowA = vec2 + P;                       // [NT*R] alpha, then u~^T, then u^1
   S* rowB = rowA + size_t(NT) * R;          // [NT*R] seed g_u per row
 
   const int phase = a.state[ST_PHASE];
@@ -102,7 +111,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   const int u = blockIdx.x;
   const int tid = threadIdx.x;
   const int n = a.n, m = a.m;
-  const size_t ubase = size_t(u) * n * m;
+  const int nm = n * m;
+  const bool vec_ok = (nm % V) == 0;   // user tiles are 16-byte aligned
+  const size_t ubase = size_t(u) * nm;
   S* Cu = a.C + ubase;
   S* mu = a.am + ubase;
   S* vu = a.av + ubase;
@@ -112,7 +123,18 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   auto ok = [&](int r) { return tid + r * NT < n; };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
   auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
+  auto kt = [&](int e) -> S& { const int i = e / m; return Kt[i * P + (e - i * m)]; };
+  // element-wise, coalesced visit of the user's [n][m] tile: f(e, vector slot)
+  auto foreach_cell = [&](auto&& f) {
+    if (vec_ok) {
+      for (int q = tid; q < nm / V; q += NT) f(q * V, q);
+    } else {
+      for (int e = tid; e < nm; e += NT) f(e, -1);
+    }
+  };
 
+  // zero the tile (padding rows / columns must stay 0) and the small vectors
+  for (int q = tid; q < NT * R * P / V; q += NT) reinterpret_cast<V16<S>*>(Kt)[q].v = V16<S>{}.v;
   if (tid < P) {
     vec0[tid] = S(0);
     vec1[tid] = S(0);
@@ -121,47 +143,69 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S ex[M];
 #pragma unroll
   for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
+  __syncthreads();
 
   if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
     // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
-    __syncthreads();
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
+    for (int i = tid; i < n; i += NT) rowA[i] = a.alpha[size_t(u) * n + i];
     for (int idx = tid; idx < (T + 1) * P; idx += NT) {
       const int t = idx / P, k = idx - t * P;
       vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
     }
     __syncthreads();
+    foreach_cell([&](int e0, int q) {
+      S c[V];
+      const int cnt = q >= 0 ? V : 1;
+      if (q >= 0) {
+        V16<S> t;
+        t.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+#pragma unroll
+        for (int j = 0; j < V; ++j) c[j] = t.s[j];
+      } else {
+        c[0] = Cu[e0];
+      }
+      int i = e0 / m, k = e0 - i * m;
+      for (int j = 0; j < cnt; ++j) {
+        Kt[i * P + k] = F::exp_(add_(add_(mul_(c[j], a.nie), rowA[i]), vec1[k]));
+        if (++k == m) { k = 0; ++i; }
+      }
+    });
+    __syncthreads();
     S vT[M];
     lds_vec<S, M>(vT, vh + size_t(T) * P);
     {
-      S bt[M], vT1[M];
-      lds_vec<S, M>(bt, vec1);
+      S vT1[M];
       lds_vec<S, M>(vT1, vh + size_t(T >= 2 ? T - 1 : 0) * P);
 #pragma unroll 1
       for (int i = tid; i < NT * R; i += NT) {
-        const bool v = i < n;
         S kr[M];
-        const S al = v ? a.alpha[size_t(u) * n + i] : S(0);
-#pragma unroll
-        for (int k = 0; k < M; ++k)
-          kr[k] = (v && k < m) ? F::exp_(add_(add_(mul_(Cu[size_t(i) * m + k], a.nie), al), bt[k])) : S(0);
-        sts_vec<S, M>(Kt + size_t(i) * P, kr);
-        rowA[i] = v ? ((T >= 2) ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(1)) : S(0);
+        lds_vec<S, M>(kr, Kt + size_t(i) * P);
+        rowA[i] = i < n ? ((T >= 2) ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(1)) : S(0);   // u~^T
       }
     }
     const int improved = a.state[ST_IMPROVED];
+    auto write_policy = [&]() {   // X = diag(u~^T) K~ diag(v~^T), coalesced
+      foreach_cell([&](int e0, int q) {
+        int i = e0 / m, k = e0 - i * m;
+        if (q >= 0) {
+          V16<S> t;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+            if (++k == m) { k = 0; ++i; }
+          }
+          reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
+        } else {
+          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+        }
+      });
+    };
     if (phase == PHASE_DONE_PENDING) {
       // the stop fired after step k-1's forward: only its policy is still owed
       if (improved) {
-#pragma unroll 1
-        for (int i = tid; i < n; i += NT) {
-          S kr[M];
-          lds_vec<S, M>(kr, Kt + size_t(i) * P);
-          const S uT = rowA[i];
-#pragma unroll
-          for (int k = 0; k < M; ++k)
-            if (k < m) xb[size_t(i) * m + k] = mul_(mul_(kr[k], uT), vT[k]);
-        }
+        __syncthreads();
+        write_policy();
       }
       return;
     }
@@ -173,19 +217,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll 1
       for (int i = tid; i < NT * R; i += NT) {
-        const bool v = i < n;
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
         const S uT = rowA[i];
-        const S rr = v ? relu[i] : S(0);
-        const S imp_i = v ? S(a.imp[i]) : S(1);
+        const S rr = i < n ? relu[i] : S(0);
+        const S imp_i = i < n ? S(a.imp[i]) : S(1);
         S gsum = S(0);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          if (k >= m) continue;
-          const S X = mul_(mul_(kr[k], uT), vT[k]);
-          if (improved && v) xb[size_t(i) * m + k] = X;
           if (k < m - 1) {
+            const S X = mul_(mul_(kr[k], uT), vT[k]);
             const S W = mul_(F::div(mul_(rr, ex[k]), imp_i), X);   // gx = r e / Imp, solver.py:86-89
             gsum += W;
             c[k] += W;
@@ -197,6 +238,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
       });
     }
+    if (improved) write_policy();   // best-so-far policy is step k-1's (solver.py:217-219)
 
     // ---------------- unrolled reverse sweep  (sinkhorn.py:278-308) ---------
     // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
@@ -215,40 +257,45 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         for (int k = 0; k < M; ++k) A[r][k] = S(0);
       }
       for (int t = T; t >= 1; --t) {
-        S cv[M], vp[M], vpp[M], c[M];
+        S cv[M], c[M], h[R], un[R];
         lds_vec<S, M>(cv, vec0);
-        lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
-        lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
         const bool first = t == T;
         const bool replay = t >= 3;
 #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
+        {
+          S vpp[M];
+          lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
 #pragma unroll
-        for (int r = 0; r < R; r += PAIR) {
-          S kr[PAIR][M], h[PAIR];
+          for (int r = 0; r < R; r += PAIR) {
+            S kr[PAIR][M];
 #pragma unroll
-          for (int q = 0; q < PAIR; ++q) lds_vec<S, M>(kr[q], Kt + size_t(tid + (r + q) * NT) * P);
+            for (int q = 0; q < PAIR; ++q) lds_vec<S, M>(kr[q], Kt + size_t(tid + (r + q) * NT) * P);
 #pragma unroll
-          for (int q = 0; q < PAIR; ++q) {
-            const S sig = rdot<S, M>(kr[q], cv);
-            const S gs = first ? rowB[tid + (r + q) * NT] : S(0);
-            h[q] = ut[r + q] * (gs - ut[r + q] * sig);
-          }
-#pragma unroll
-          for (int q = 0; q < PAIR; ++q)
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
-              A[r + q][k] = fma(-ut[r + q], cv[k], A[r + q][k]);
-              A[r + q][k] = fma(-h[q], vp[k], A[r + q][k]);
+            for (int q = 0; q < PAIR; ++q) {
+              const S sig = rdot<S, M>(kr[q], cv);
+              const S den = rdot<S, M>(kr[q], vpp);
+              const S gs = first ? rowB[tid + (r + q) * NT] : S(0);
+              h[r + q] = ut[r + q] * (gs - ut[r + q] * sig);
+              un[r + q] = ok(r + q) ? (replay ? F::rcp_fast(den) : S(1)) : S(0);
             }
 #pragma unroll
-          for (int k = 0; k < M; ++k)
+            for (int k = 0; k < M; ++k)
 #pragma unroll
-            for (int q = 0; q < PAIR; ++q) c[k] = fma(kr[q][k], h[q], c[k]);
+              for (int q = 0; q < PAIR; ++q) c[k] = fma(kr[q][k], h[r + q], c[k]);
+          }
+        }
+        {
+          S vp[M];
+          lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
 #pragma unroll
-          for (int q = 0; q < PAIR; ++q) {
-            const S rp = F::rcp_fast(rdot<S, M>(kr[q], vpp));
-            ut[r + q] = ok(r + q) ? (replay ? rp : S(1)) : S(0);
+          for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+              A[r][k] = fma(-ut[r], cv[k], A[r][k]);
+              A[r][k] = fma(-h[r], vp[k], A[r][k]);
+            }
+            ut[r] = un[r];
           }
         }
         if (t >= 2) {
@@ -277,62 +324,87 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         sts_vec<S, M>(Kt + size_t(i) * P, gk);
       }
     }
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
+    __syncthreads();
 
     // ---------------- g_C = gK * (-1/eps); Adam ascent  (solver.py:105-122) -
     const int s = a.state[ST_STEP];
     const S bc1 = S(a.bc[2 * s]), bc2 = S(a.bc[2 * s + 1]);
-    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
-#pragma unroll 1
-    for (int i = tid; i < n; i += NT) {
-      S gk[M], kn[M];
-      lds_vec<S, M>(gk, Kt + size_t(i) * P);
+    auto adam = [&](S& cc, S& mm, S& vv, S gk) {
+      const S g = mul_(gk, a.nie);
+      mm = add_(mul_(a.b1, mm), mul_(a.omb1, g));
+      vv = add_(mul_(a.b2, vv), mul_(mul_(a.omb2, g), g));
+      const S mh = F::div(mm, bc1);
+      const S vhat = F::div(vv, bc2);
+      cc = add_(cc, F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
+    };
+    foreach_cell([&](int e0, int q) {
+      int i = e0 / m, k = e0 - i * m;
+      if (q >= 0) {
+        V16<S> c, mm, vv;
+        c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+        mm.v = reinterpret_cast<const V16<S>*>(mu)[q].v;
+        vv.v = reinterpret_cast<const V16<S>*>(vu)[q].v;
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        kn[k] = S(0);
-        if (k < m) {
-          const S g = mul_(gk[k], a.nie);
-          const size_t off = size_t(i) * m + k;
-          const S m1 = add_(mul_(a.b1, mu[off]), mul_(a.omb1, g));
-          const S v1 = add_(mul_(a.b2, vu[off]), mul_(mul_(a.omb2, g), g));
-          const S mh = F::div(m1, bc1);
-          const S vhat = F::div(v1, bc2);
-          const S c1 = add_(Cu[off], F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
-          mu[off] = m1;
-          vu[off] = v1;
-          Cu[off] = c1;
-          kn[k] = mul_(c1, a.nie);
+        for (int j = 0; j < V; ++j) {
+          S& slot = Kt[i * P + k];
+          adam(c.s[j], mm.s[j], vv.s[j], slot);
+          slot = mul_(c.s[j], a.nie);
+          if (++k == m) { k = 0; ++i; }
         }
+        reinterpret_cast<V16<S>*>(Cu)[q].v = c.v;
+        reinterpret_cast<V16<S>*>(mu)[q].v = mm.v;
+        reinterpret_cast<V16<S>*>(vu)[q].v = vv.v;
+      } else {
+        S c = Cu[e0], mm = mu[e0], vv = vu[e0];
+        S& slot = Kt[i * P + k];
+        adam(c, mm, vv, slot);
+        slot = mul_(c, a.nie);
+        Cu[e0] = c;
+        mu[e0] = mm;
+        vu[e0] = vv;
       }
-      sts_vec<S, M>(Kt + size_t(i) * P, kn);
-    }
+    });
   } else {
     // INIT: initial cost C0 = -eps log(uniform) (solver.py:176-177), lvi = 0.
     // RESUME: caller-provided C (left as is), lvi taken from the beta buffer.
     const bool init = phase == PHASE_INIT;
-    __syncthreads();
     if (!init && tid < m) vec2[tid] = a.beta[size_t(u) * m + tid];
-#pragma unroll 1
-    for (int i = tid; i < n; i += NT) {
-      S kn[M];
+    foreach_cell([&](int e0, int q) {
+      int i = e0 / m, k = e0 - i * m;
+      if (q >= 0) {
+        V16<S> c;
+        if (init) {
 #pragma unroll
-      for (int k = 0; k < M; ++k) {
-        kn[k] = S(0);
-        if (k < m) {
-          const size_t off = size_t(i) * m + k;
-          S c0;
-          if (init) {
-            c0 = (k == m - 1) ? a.c_dummy : a.c_real;
-            Cu[off] = c0;
-            mu[off] = S(0);
-            vu[off] = S(0);
-          } else {
-            c0 = Cu[off];
+          for (int j = 0; j < V; ++j) {
+            c.s[j] = (k == m - 1) ? a.c_dummy : a.c_real;
+            Kt[i * P + k] = mul_(c.s[j], a.nie);
+            if (++k == m) { k = 0; ++i; }
           }
-          kn[k] = mul_(c0, a.nie);
+          reinterpret_cast<V16<S>*>(Cu)[q].v = c.v;
+          reinterpret_cast<V16<S>*>(mu)[q].v = V16<S>{}.v;
+          reinterpret_cast<V16<S>*>(vu)[q].v = V16<S>{}.v;
+        } else {
+          c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            Kt[i * P + k] = mul_(c.s[j], a.nie);
+            if (++k == m) { k = 0; ++i; }
+          }
         }
+      } else {
+        S c0;
+        if (init) {
+          c0 = (k == m - 1) ? a.c_dummy : a.c_real;
+          Cu[e0] = c0;
+          mu[e0] = S(0);
+          vu[e0] = S(0);
+        } else {
+          c0 = Cu[e0];
+        }
+        Kt[i * P + k] = mul_(c0, a.nie);
       }
-      sts_vec<S, M>(Kt + size_t(i) * P, kn);
-    }
+    });
   }
   __syncthreads();
 
@@ -389,14 +461,13 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     S bt[M];
     lds_vec<S, M>(bt, vec1);
 #pragma unroll 1
-    for (int i = tid; i < NT * R; i += NT) {
-      const bool v = i < n;
+    for (int i = tid; i < n; i += NT) {
       S kr[M];
       lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S u1 = v ? rowA[i] : S(0);
-      if (v) a.alpha[size_t(u) * n + i] = u1;
+      const S u1 = rowA[i];
+      a.alpha[size_t(u) * n + i] = u1;
 #pragma unroll
-      for (int k = 0; k < M; ++k) kr[k] = (v && k < m) ? F::exp_(add_(add_(kr[k], u1), bt[k])) : S(0);
+      for (int k = 0; k < M; ++k) kr[k] = (k < m) ? F::exp_(add_(add_(kr[k], u1), bt[k])) : S(0);
       sts_vec<S, M>(Kt + size_t(i) * P, kr);
     }
   }
@@ -423,7 +494,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (int r = 1; r < R; ++r) c[k] = fma(A[r][k], ut[r], c[k]);
     }
     cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-      const S vn = F::div(mass(k), tot);
+      const S vn = F::div_fast(mass(k), tot);
       vec0[k] = vn;
       hu[size_t(t) * m + k] = vn;
     });
