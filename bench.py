@@ -241,9 +241,9 @@ def run_ours(a):
     from paper_2406_10262_b200.solver import DeviceSolver, solve_fair_ranking
 
     cfg = BASELINE_CONFIGS[a.config]
-    rel, expo, _ = make_instance(a.config, seed=0)
-    U, n, m, T = cfg.num_users, cfg.num_items, cfg.num_positions, cfg.inner_iters
-    opts = DeviceOptions(dtype=a.dtype, device=local)
+    rel, expo, _ = make_instance(a.config, seed=0, num_users=a.users)
+    U, n, m, T = rel.shape[0], cfg.num_items, cfg.num_positions, a.inner or cfg.inner_iters
+    opts = DeviceOptions(dtype=a.dtype, device=local, variant=a.variant)
     scfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=a.warmup + a.steps + 2,
                         grad_threshold=1e-300)
     peaks, peaks_kind = _peaks()
@@ -369,6 +369,10 @@ def main(argv=None):
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    # experiment knobs (not used by the driver): override |U|, inner iterations, tile variant
+    ap.add_argument("--users", type=int, default=None)
+    ap.add_argument("--inner", type=int, default=None)
+    ap.add_argument("--variant", type=int, default=-1)
     a = ap.parse_args(argv)
     if a.dtype is None:
         a.dtype = BASELINE_CONFIGS[a.config].dtype

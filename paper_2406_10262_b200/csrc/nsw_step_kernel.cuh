@@ -22,9 +22,9 @@ struct StepArgs {
   S* C;          // [U][n][m] transport costs (the ascent variable)
   S* am;         // [U][n][m] Adam first moment
   S* av;         // [U][n][m] Adam second moment
-  S* alpha;      // [U][n]    row dual after inner iteration 1 (absorption point)
-  S* beta;       // [U][m]    column dual after inner iteration 1
-  S* hist;       // [U][T+1][m] v~^t, t = 0..T  (v~^0 = exp(lvi - beta), v~^1 = 1)
+  S* alpha;      // [U][n]    row absorption point -max_k(K_ik + beta_k)
+  S* beta;       // [U][m]    column absorption point = warm-start duals lvi
+  S* hist;       // [U][T+1][m] v~^t = exp(v^t - beta), t = 0..T (v~^0 = 1)
   S* xbest;      // [U][n][m] best-F policy so far
   const S* rel;          // [U][n]
   const S* expo;         // [m-1]
@@ -74,26 +74,54 @@ union V16 {
   S s[16 / sizeof(S)];
 };
 
+// Per-row scalars (alpha, u~^T, seed g_u, u^1) live in the tile's padding
+// column when the row pitch has one (P > M), else in two row buffers.
+template <typename S, int M>
+struct RowSlots {
+  static constexpr int P = Pitch<S, M>::value;
+  static constexpr bool kPad = P > M;
+};
+
 template <typename S, int M, int R, int NT>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
-  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + 2 * size_t(NT) * R);
+  constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
+  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows);
+}
+
+// fp32 throughput path: divisions / square roots off the hot path use the
+// fast (MUFU) forms; the fp64 parity path keeps IEEE-rounded operations in
+// the reference's order (solver.py:86-89, :115-121).
+template <typename S>
+__device__ __forceinline__ S fdiv_(S a, S b) {
+  if constexpr (sizeof(S) == 4) return Fp<float>::div_fast(a, b);
+  else return Fp<double>::div(a, b);
+}
+template <typename S>
+__device__ __forceinline__ S fsqrt_(S x) {
+  if constexpr (sizeof(S) == 4) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+  } else {
+    return Fp<double>::sqrt_(x);
+  }
 }
 
 // Structure: the per-step phases that touch every cell once move the user's
 // contiguous [n][m] tiles between HBM and the shared-memory tile Kt with
 // coalesced 16-byte accesses (element-wise phases: K~ rebuild, Adam, the
-// policy write) or as runtime loops over this thread's rows (seed, log-domain
+// policy write) or as loops over this thread's rows (seed, log-domain
 // iteration 1); only the two hot loops (forward iterations 2..T and the T
 // reverse levels) hold the R x M tile in registers.
 template <typename S, int M, int R, int NT, int MINB>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   using F = Fp<S>;
   constexpr int P = Pitch<S, M>::value;
+  constexpr bool PAD = RowSlots<S, M>::kPad;
   constexpr int NW = NT / 32;
   constexpr int V = 16 / sizeof(S);
-  constexpr int PAIR = R >= 2 ? 2 : 1;
-  static_assert(NT % 32 == 0 && M <= NT && P <= NT && R % PAIR == 0, "tile shape");
+  static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K / K~ / gK rows
@@ -102,8 +130,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* vec0 = red + NW * P;                   // [P] scaling vector / cv
   S* vec1 = vec0 + P;                       // [P] beta / column max
   S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
-  S* rowA = vec2 + P;                       // [NT*R] alpha, then u~^T, then u^1
-  S* rowB = rowA + size_t(NT) * R;          // [NT*R] seed g_u per row
+  S* rowA = vec2 + P;                       // [NT*R] (no padding column only)
+  S* rowB = rowA + size_t(NT) * R;
+  // slotA: alpha -> u~^T -> u^1 ; slotB: seed g_u (shares slotA's storage
+  // when PAD: written after u~^T is in registers, u~^T restored at level T)
+  auto slotA = [&](int i) -> S& { return PAD ? Kt[size_t(i) * P + M] : rowA[i]; };
+  auto slotB = [&](int i) -> S& { return PAD ? Kt[size_t(i) * P + M] : rowB[i]; };
 
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) return;
@@ -121,18 +153,37 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* hu = a.hist + size_t(u) * (T + 1) * m;
   const S* relu = a.rel + size_t(u) * n;
   auto ok = [&](int r) { return tid + r * NT < n; };
+  // K~ = exp(K + beta_k + alpha_i), K = C * (-1/eps) (solver.py:188); the one
+  // expression used by both the forward and the backward's rebuild, so K~ is
+  // bit-identical in both.
+  auto ktilde = [&](S c, S beta_k, S alpha_i) -> S {
+    return F::exp_fast(add_(add_(mul_(c, a.nie), beta_k), alpha_i));
+  };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
   auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
-  auto kt = [&](int e) -> S& { const int i = e / m; return Kt[i * P + (e - i * m)]; };
-  // element-wise, coalesced visit of the user's [n][m] tile: f(e, vector slot)
-  auto foreach_cell = [&](auto&& f) {
-    if (vec_ok) {
-      for (int q = tid; q < nm / V; q += NT) f(q * V, q);
-    } else {
-      for (int e = tid; e < nm; e += NT) f(e, -1);
-    }
+  // gx = r e / Imp (solver.py:86-89); fp32 uses a per-row reciprocal
+  auto gx_of = [&](S rr, S e, S imp_i, S inv_imp) -> S {
+    if constexpr (sizeof(S) == 4) return mul_(mul_(rr, e), inv_imp);
+    else return F::div(mul_(rr, e), imp_i);
   };
 
+  // warm L2 with this user's tiles (C, Adam moments, duals, history,
+  // relevance): one prefetch per 128-byte line, spread over the CTA.
+  {
+    auto pf = [&](const void* base, size_t bytes) {
+      const char* b = reinterpret_cast<const char*>(base);
+      for (size_t off = size_t(tid) * 128; off < bytes; off += size_t(NT) * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b + off));
+    };
+    pf(Cu, size_t(nm) * sizeof(S));
+    if (phase == PHASE_RUNNING) {
+      pf(mu, size_t(nm) * sizeof(S));
+      pf(vu, size_t(nm) * sizeof(S));
+    }
+    pf(hu, size_t(T + 1) * m * sizeof(S));
+    pf(a.alpha + size_t(u) * n, size_t(n) * sizeof(S));
+    pf(relu, size_t(n) * sizeof(S));
+  }
   // zero the tile (padding rows / columns must stay 0) and the small vectors
   for (int q = tid; q < NT * R * P / V; q += NT) reinterpret_cast<V16<S>*>(Kt)[q].v = V16<S>{}.v;
   if (tid < P) {
@@ -148,58 +199,75 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
     // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
-    for (int i = tid; i < n; i += NT) rowA[i] = a.alpha[size_t(u) * n + i];
-    for (int idx = tid; idx < (T + 1) * P; idx += NT) {
-      const int t = idx / P, k = idx - t * P;
-      vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
+    for (int i = tid; i < n; i += NT) slotA(i) = a.alpha[size_t(u) * n + i];
+    for (int idx0 = tid; idx0 < (T + 1) * P; idx0 += 4 * NT) {
+      S hv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int idx = idx0 + j * NT;
+        const int t = idx / P, k = idx - t * P;
+        hv[j] = (idx < (T + 1) * P && k < m) ? hu[size_t(t) * m + k] : S(0);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (idx0 + j * NT < (T + 1) * P) vh[idx0 + j * NT] = hv[j];
     }
     __syncthreads();
-    foreach_cell([&](int e0, int q) {
-      S c[V];
-      const int cnt = q >= 0 ? V : 1;
-      if (q >= 0) {
-        V16<S> t;
-        t.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+    if (vec_ok) {
+      const int nq = nm / V;
+      for (int q0 = tid; q0 < nq; q0 += 4 * NT) {
+        V16<S> c[4];
 #pragma unroll
-        for (int j = 0; j < V; ++j) c[j] = t.s[j];
-      } else {
-        c[0] = Cu[e0];
+        for (int b = 0; b < 4; ++b)
+          if (q0 + b * NT < nq) c[b].v = reinterpret_cast<const V16<S>*>(Cu)[q0 + b * NT].v;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int q = q0 + b * NT;
+          if (q >= nq) break;
+          int i = q * V / m, k = q * V - i * m;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            Kt[i * P + k] = ktilde(c[b].s[j], vec1[k], slotA(i));
+            if (++k == m) { k = 0; ++i; }
+          }
+        }
       }
-      int i = e0 / m, k = e0 - i * m;
-      for (int j = 0; j < cnt; ++j) {
-        Kt[i * P + k] = F::exp_(add_(add_(mul_(c[j], a.nie), rowA[i]), vec1[k]));
-        if (++k == m) { k = 0; ++i; }
+    } else {
+      for (int e = tid; e < nm; e += NT) {
+        const int i = e / m, k = e - i * m;
+        Kt[i * P + k] = ktilde(Cu[e], vec1[k], slotA(i));
       }
-    });
+    }
     __syncthreads();
     S vT[M];
     lds_vec<S, M>(vT, vh + size_t(T) * P);
     {
       S vT1[M];
-      lds_vec<S, M>(vT1, vh + size_t(T >= 2 ? T - 1 : 0) * P);
+      lds_vec<S, M>(vT1, vh + size_t(T - 1) * P);
 #pragma unroll 1
       for (int i = tid; i < NT * R; i += NT) {
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        rowA[i] = i < n ? ((T >= 2) ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(1)) : S(0);   // u~^T
+        slotA(i) = i < n ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(0);   // u~^T
       }
     }
     const int improved = a.state[ST_IMPROVED];
     auto write_policy = [&]() {   // X = diag(u~^T) K~ diag(v~^T), coalesced
-      foreach_cell([&](int e0, int q) {
+      for (int q = tid; q < (vec_ok ? nm / V : nm); q += NT) {
+        const int e0 = vec_ok ? q * V : q;
         int i = e0 / m, k = e0 - i * m;
-        if (q >= 0) {
+        if (vec_ok) {
           V16<S> t;
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+            t.s[j] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(T) * P + k]);
             if (++k == m) { k = 0; ++i; }
           }
           reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
         } else {
-          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+          xb[e0] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(T) * P + k]);
         }
-      });
+      }
     };
     if (phase == PHASE_DONE_PENDING) {
       // the stop fired after step k-1's forward: only its policy is still owed
@@ -209,120 +277,110 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       }
       return;
     }
+    __syncthreads();
+    if (improved) write_policy();   // best-so-far policy is step k-1's (solver.py:217-219)
+    __syncthreads();
 
     // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
+    S A[R][M];  // adjoint G: gK = W + K~ .* G
+    S ut[R];
     {
       S c[M];
 #pragma unroll
       for (int k = 0; k < M; ++k) c[k] = S(0);
-#pragma unroll 1
-      for (int i = tid; i < NT * R; i += NT) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        const S uT = rowA[i];
-        const S rr = i < n ? relu[i] : S(0);
-        const S imp_i = i < n ? S(a.imp[i]) : S(1);
+        ut[r] = slotA(i);
+        const S rr = ok(r) ? relu[i] : S(0);
+        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+        const S inv_imp = S(1.0 / double(imp_i));
         S gsum = S(0);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
+          A[r][k] = S(0);
           if (k < m - 1) {
-            const S X = mul_(mul_(kr[k], uT), vT[k]);
-            const S W = mul_(F::div(mul_(rr, ex[k]), imp_i), X);   // gx = r e / Imp, solver.py:86-89
+            const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
+            const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), X);
             gsum += W;
             c[k] += W;
           }
         }
-        rowB[i] = gsum;
+        slotB(i) = gsum;
       }
       cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
         vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
       });
     }
-    if (improved) write_policy();   // best-so-far policy is step k-1's (solver.py:217-219)
 
-    // ---------------- unrolled reverse sweep  (sinkhorn.py:278-308) ---------
     // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
     //   g_u  <- [t==T] g_u^seed - u~ (K~ cv)_i                  column VJP
     //   h    <- u~ g_u
     //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
     //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
-    //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 3)
-    {
-      S A[R][M];  // adjoint G: gK = W + K~ .* G
-      S ut[R];
+    //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 2)
+    for (int t = T; t >= 1; --t) {
+      S cv[M], vp[M], c[M];
+      lds_vec<S, M>(cv, vec0);
+      lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
+      const S* vppp = vh + size_t(t >= 2 ? t - 2 : 0) * P;
+      const bool first = t == T;
+      const bool replay = t >= 2;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        ut[r] = rowA[tid + r * NT];
-#pragma unroll
-        for (int k = 0; k < M; ++k) A[r][k] = S(0);
-      }
-      for (int t = T; t >= 1; --t) {
-        S cv[M], c[M], h[R], un[R];
-        lds_vec<S, M>(cv, vec0);
-        const bool first = t == T;
-        const bool replay = t >= 3;
-#pragma unroll
-        for (int k = 0; k < M; ++k) c[k] = S(0);
-        {
-          S vpp[M];
-          lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
-#pragma unroll
-          for (int r = 0; r < R; r += PAIR) {
-            S kr[PAIR][M];
-#pragma unroll
-            for (int q = 0; q < PAIR; ++q) lds_vec<S, M>(kr[q], Kt + size_t(tid + (r + q) * NT) * P);
-#pragma unroll
-            for (int q = 0; q < PAIR; ++q) {
-              const S sig = rdot<S, M>(kr[q], cv);
-              const S den = rdot<S, M>(kr[q], vpp);
-              const S gs = first ? rowB[tid + (r + q) * NT] : S(0);
-              h[r + q] = ut[r + q] * (gs - ut[r + q] * sig);
-              un[r + q] = ok(r + q) ? (replay ? F::rcp_fast(den) : S(1)) : S(0);
-            }
-#pragma unroll
-            for (int k = 0; k < M; ++k)
-#pragma unroll
-              for (int q = 0; q < PAIR; ++q) c[k] = fma(kr[q][k], h[r + q], c[k]);
-          }
-        }
-        {
-          S vp[M];
-          lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-#pragma unroll
-            for (int k = 0; k < M; ++k) {
-              A[r][k] = fma(-ut[r], cv[k], A[r][k]);
-              A[r][k] = fma(-h[r], vp[k], A[r][k]);
-            }
-            ut[r] = un[r];
-          }
-        }
-        if (t >= 2) {
-          cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-            const S vpk = vh[size_t(t - 1) * P + k];
-            const S gv = -mul_(vpk, tot);
-            vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
-          });
-        }
-      }
-      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
+      for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
-        S kr[M], gk[M];
+        S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        const S uT = rowA[i];
-        const S rr = ok(r) ? relu[i] : S(0);
-        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+        const S sig = rdot<S, M>(kr, cv);
+        S den;
+        {
+          S vpp[M];
+          lds_vec<S, M>(vpp, vppp);
+          den = rdot<S, M>(kr, vpp);
+        }
+        S gs = S(0);
+        if (first) {
+          gs = slotB(i);
+          slotA(i) = ut[r];   // restore u~^T for the gK epilogue
+        }
+        const S h = ut[r] * (gs - ut[r] * sig);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const S X = mul_(mul_(kr[k], uT), vT[k]);
-          const S W = (k < m - 1) ? mul_(F::div(mul_(rr, ex[k]), imp_i), X) : S(0);
-          gk[k] = fma(kr[k], A[r][k], W);
+          A[r][k] = fma(-ut[r], cv[k], A[r][k]);
+          A[r][k] = fma(-h, vp[k], A[r][k]);
+          c[k] = fma(kr[k], h, c[k]);
         }
-        sts_vec<S, M>(Kt + size_t(i) * P, gk);
+        ut[r] = (ok(r) && replay) ? F::rcp_fast(den) : S(0);
       }
+      if (t >= 2) {
+        cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+          const S vpk = vh[size_t(t - 1) * P + k];
+          const S gv = -mul_(vpk, tot);
+          vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+        });
+      }
+    }
+    // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = tid + r * NT;
+      S kr[M], gk[M];
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      const S uT = slotA(i);
+      const S rr = ok(r) ? relu[i] : S(0);
+      const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+      const S inv_imp = S(1.0 / double(imp_i));
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const S X = mul_(mul_(kr[k], uT), vT[k]);
+        const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), X) : S(0);
+        gk[k] = fma(kr[k], A[r][k], W);
+      }
+      sts_vec<S, M>(Kt + size_t(i) * P, gk);
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
     __syncthreads();
@@ -330,49 +388,72 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     // ---------------- g_C = gK * (-1/eps); Adam ascent  (solver.py:105-122) -
     const int s = a.state[ST_STEP];
     const S bc1 = S(a.bc[2 * s]), bc2 = S(a.bc[2 * s + 1]);
+    const S ibc1 = S(1.0 / a.bc[2 * s]), ibc2 = S(1.0 / a.bc[2 * s + 1]);
     auto adam = [&](S& cc, S& mm, S& vv, S gk) {
       const S g = mul_(gk, a.nie);
       mm = add_(mul_(a.b1, mm), mul_(a.omb1, g));
       vv = add_(mul_(a.b2, vv), mul_(mul_(a.omb2, g), g));
-      const S mh = F::div(mm, bc1);
-      const S vhat = F::div(vv, bc2);
-      cc = add_(cc, F::div(mul_(a.lr, mh), add_(F::sqrt_(vhat), a.aeps)));
-    };
-    foreach_cell([&](int e0, int q) {
-      int i = e0 / m, k = e0 - i * m;
-      if (q >= 0) {
-        V16<S> c, mm, vv;
-        c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
-        mm.v = reinterpret_cast<const V16<S>*>(mu)[q].v;
-        vv.v = reinterpret_cast<const V16<S>*>(vu)[q].v;
-#pragma unroll
-        for (int j = 0; j < V; ++j) {
-          S& slot = Kt[i * P + k];
-          adam(c.s[j], mm.s[j], vv.s[j], slot);
-          slot = mul_(c.s[j], a.nie);
-          if (++k == m) { k = 0; ++i; }
-        }
-        reinterpret_cast<V16<S>*>(Cu)[q].v = c.v;
-        reinterpret_cast<V16<S>*>(mu)[q].v = mm.v;
-        reinterpret_cast<V16<S>*>(vu)[q].v = vv.v;
+      S mh, vhat;
+      if constexpr (sizeof(S) == 4) {
+        mh = mul_(mm, ibc1);
+        vhat = mul_(vv, ibc2);
       } else {
-        S c = Cu[e0], mm = mu[e0], vv = vu[e0];
+        mh = F::div(mm, bc1);
+        vhat = F::div(vv, bc2);
+      }
+      cc = add_(cc, fdiv_<S>(mul_(a.lr, mh), add_(fsqrt_<S>(vhat), a.aeps)));
+    };
+    if (vec_ok) {
+      const int nq = nm / V;
+      for (int q0 = tid; q0 < nq; q0 += 2 * NT) {
+        V16<S> c[2], mm[2], vv[2];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int q = q0 + b * NT;
+          if (q < nq) {
+            c[b].v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+            mm[b].v = reinterpret_cast<const V16<S>*>(mu)[q].v;
+            vv[b].v = reinterpret_cast<const V16<S>*>(vu)[q].v;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int q = q0 + b * NT;
+          if (q >= nq) break;
+          int i = q * V / m, k = q * V - i * m;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            S& slot = Kt[i * P + k];
+            adam(c[b].s[j], mm[b].s[j], vv[b].s[j], slot);
+            slot = mul_(c[b].s[j], a.nie);
+            if (++k == m) { k = 0; ++i; }
+          }
+          reinterpret_cast<V16<S>*>(Cu)[q].v = c[b].v;
+          reinterpret_cast<V16<S>*>(mu)[q].v = mm[b].v;
+          reinterpret_cast<V16<S>*>(vu)[q].v = vv[b].v;
+        }
+      }
+    } else {
+      for (int e = tid; e < nm; e += NT) {
+        const int i = e / m, k = e - i * m;
+        S c = Cu[e], mm = mu[e], vv = vu[e];
         S& slot = Kt[i * P + k];
         adam(c, mm, vv, slot);
         slot = mul_(c, a.nie);
-        Cu[e0] = c;
-        mu[e0] = mm;
-        vu[e0] = vv;
+        Cu[e] = c;
+        mu[e] = mm;
+        vu[e] = vv;
       }
-    });
+    }
   } else {
     // INIT: initial cost C0 = -eps log(uniform) (solver.py:176-177), lvi = 0.
     // RESUME: caller-provided C (left as is), lvi taken from the beta buffer.
     const bool init = phase == PHASE_INIT;
     if (!init && tid < m) vec2[tid] = a.beta[size_t(u) * m + tid];
-    foreach_cell([&](int e0, int q) {
+    for (int q = tid; q < (vec_ok ? nm / V : nm); q += NT) {
+      const int e0 = vec_ok ? q * V : q;
       int i = e0 / m, k = e0 - i * m;
-      if (q >= 0) {
+      if (vec_ok) {
         V16<S> c;
         if (init) {
 #pragma unroll
@@ -404,82 +485,46 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         }
         Kt[i * P + k] = mul_(c0, a.nie);
       }
-    });
+    }
   }
   __syncthreads();
 
   // ======================= forward of step k =================================
-  // inner iteration 1 in the log domain (sinkhorn.py:219-234), v^0 = lvi;
-  // K = C * (-1/eps) is in the tile rows i < n.
+  // Absorption point: beta = lvi (the warm-start column duals, so v~^0 = 1)
+  // and alpha_i = -max_k (K_ik + beta_k), so every K~ row peaks at exactly 1.
+  // Then iterations t = 1..T are the multiplicative Sinkhorn updates, the
+  // same fixed point as the log-domain iterations of sinkhorn.py:219-234:
+  //   u~^t = 1 / (K~ v~^{t-1}),   v~^t = colmass / (K~' u~^t),
+  //   u^t = alpha + log u~^t,     v^t = beta + log v~^t.
+  if (tid < m) {
+    a.beta[size_t(u) * m + tid] = vec2[tid];
+    hu[tid] = S(1);                       // v~^0
+    vec0[tid] = S(1);
+  }
   {
-    S lv[M], c[M];
-    lds_vec<S, M>(lv, vec2);
-#pragma unroll
-    for (int k = 0; k < M; ++k) c[k] = F::ninf();
+    S bt[M];
+    lds_vec<S, M>(bt, vec2);
 #pragma unroll 1
     for (int i = tid; i < n; i += NT) {
       S kr[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
+      lds_vec<S, M>(kr, Kt + size_t(i) * P);   // K = C * (-1/eps)
       S mx = F::ninf();
 #pragma unroll
       for (int k = 0; k < M; ++k)
-        if (k < m) mx = fmax(mx, add_(kr[k], lv[k]));
-      S acc = S(0);
+        if (k < m) mx = fmax(mx, add_(kr[k], bt[k]));
+      const S al = -mx;
+      a.alpha[size_t(u) * n + i] = al;
 #pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k < m) acc += F::exp_(add_(kr[k], lv[k]) - mx);
-      const S u1 = -(F::log_(acc) + mx);
-      rowA[i] = u1;
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k < m) c[k] = fmax(c[k], add_(kr[k], u1));
-    }
-    cta_reduce_cols<S, M, NT, OpMax>(c, red, m, [&](int k, S tot) { vec1[k] = tot; });
-    S cm[M];
-    lds_vec<S, M>(cm, vec1);
-#pragma unroll
-    for (int k = 0; k < M; ++k) c[k] = S(0);
-#pragma unroll 1
-    for (int i = tid; i < n; i += NT) {
-      S kr[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S u1 = rowA[i];
-#pragma unroll
-      for (int k = 0; k < M; ++k)
-        if (k < m) c[k] += F::exp_(add_(kr[k], u1) - cm[k]);
-    }
-    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-      const S lc = (k == m - 1) ? a.log_mass_dummy : S(0);
-      const S b = lc - (F::log_(tot) + vec1[k]);
-      vec1[k] = b;
-      a.beta[size_t(u) * m + k] = b;
-      hu[k] = F::exp_(vec2[k] - b);  // v~^0
-      if (T >= 1) hu[size_t(1) * m + k] = S(1);  // v~^1
-      vec0[k] = S(1);
-    });
-    // absorb: K~ = exp(K + u^1 + v^1) = X^1 (rows >= n stay zero)
-    S bt[M];
-    lds_vec<S, M>(bt, vec1);
-#pragma unroll 1
-    for (int i = tid; i < n; i += NT) {
-      S kr[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S u1 = rowA[i];
-      a.alpha[size_t(u) * n + i] = u1;
-#pragma unroll
-      for (int k = 0; k < M; ++k) kr[k] = (k < m) ? F::exp_(add_(add_(kr[k], u1), bt[k])) : S(0);
+      for (int k = 0; k < M; ++k) kr[k] = (k < m) ? F::exp_fast(add_(add_(kr[k], bt[k]), al)) : S(0);
       sts_vec<S, M>(Kt + size_t(i) * P, kr);
     }
   }
-  // inner iterations 2..T, multiplicative: u~ = 1/(K~ v~), v~ = colmass/(K~' u~)
+  __syncthreads();
   S A[R][M];  // K~, register resident
   S ut[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    lds_vec<S, M>(A[r], Kt + size_t(tid + r * NT) * P);
-    ut[r] = ok(r) ? S(1) : S(0);
-  }
-  for (int t = 2; t <= T; ++t) {
+  for (int r = 0; r < R; ++r) lds_vec<S, M>(A[r], Kt + size_t(tid + r * NT) * P);
+  for (int t = 1; t <= T; ++t) {
     S vv[M], c[M];
     lds_vec<S, M>(vv, vec0);
 #pragma unroll
