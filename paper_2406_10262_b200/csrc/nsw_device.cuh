@@ -2,19 +2,20 @@
 //
 // Data layout in HBM (per GPU, users are this rank's contiguous block):
 //   C, adam_m, adam_v, xbest : [U][n][m]   reference layout (solver.py:176-185)
-//   alpha                    : [U][n]      row dual after inner iteration 1
-//   beta                     : [U][m]      column dual after inner iteration 1
+//   alpha                    : [U][n]      row absorption point
+//   beta                     : [U][m]      column absorption point (= lvi)
 //   hist                     : [U][T+1][m] v~^t = exp(v^t - beta), t = 0..T
 //   partial                  : [U][n] f64  per-user impact terms
 //
 // Numerical form ("stabilised multiplicative"):
-// iteration 1 of every solve runs in the log domain exactly like the
-// reference (sinkhorn.py:219-234); its duals (alpha, beta) are absorbed into
-// K~ = exp(K + alpha 1' + 1 beta') = X^1, a properly scaled plan in [0, 1],
-// and iterations 2..T are u~ = 1/(K~ v~), v~ = colmass/(K~' u~) -- two FMAs
-// per cell and one reciprocal per row / column, with K~ held in registers.
+// every solve absorbs beta = lvi (the warm-start column duals of
+// sinkhorn.py:213, so v~^0 = 1) and alpha_i = -max_k (K_ik + beta_k) into
+// K~ = exp(K + alpha 1' + 1 beta') <= 1, then runs the T iterations of
+// sinkhorn.py:218-236 as u~ = 1/(K~ v~), v~ = colmass/(K~' u~) -- two FMAs
+// per cell and one reciprocal per row / column, with K~ held in registers;
+// u = alpha + log u~, v = beta + log v~ are the reference's log-domain duals.
 // The unrolled reverse mode (sinkhorn.py:258-309) is restated in the same
-// coordinates (see step_kernel below).
+// coordinates (see step_kernel in nsw_step_kernel.cuh).
 #pragma once
 
 #include <cuda_runtime.h>
