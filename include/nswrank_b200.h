@@ -141,8 +141,11 @@ nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, 
 nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value);
 /* Number of kernel launches issued by the solver so far (evidence counter). */
 int64_t nsw_solver_launch_count(nsw_solver* s);
-/* Kernel variant chosen for the fused step: M, rows/thread, threads/CTA. */
+/* Kernel variant chosen for the fused step: M, rows/thread, threads/CTA of the
+ * main launch; a tail launch's R / NT (if any) are packed in bits 16..31. */
 nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT, int32_t* smem_bytes);
+/* Users handled by the tail launch (the wide, latency-oriented tile). */
+int32_t nsw_solver_tail_users(nsw_solver* s);
 /* Device time (ms) of the last N fused step kernels, CUDA events. */
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused_kernel);

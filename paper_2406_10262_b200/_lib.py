@@ -67,7 +67,8 @@ SIGNATURES = {
     "nsw_solver_set_scalar": (C.c_int, [_vp, C.c_char_p, C.c_int64]),
     "nsw_solver_launch_count": (C.c_int64, [_vp]),
     "nsw_solver_variant": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
-    "nsw_solver_time_steps": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "nsw_solver_tail_users": (_i32, [_vp]),
+    "nsw_solver_time_steps":(C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "nsw_sinkhorn_batch_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_batch_f32": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_backward_batch_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),

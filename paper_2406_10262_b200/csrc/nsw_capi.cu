@@ -71,6 +71,18 @@ const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
   return c[0];
 }
 
+// Latency-oriented tile for a launch with at most one user per SM: same M,
+// about two rows per thread (short serial chains, cheap cross-warp sums),
+// then the fewest threads that cover n.
+const Variant* choose_wide_variant(const Variant* base, int n, int T) {
+  const Variant* best = nullptr;
+  auto score = [](const Variant* v) { return std::abs(v->R - 2) * 4096 + v->NT; };
+  for (auto& v : variant_registry())
+    if (v.dtype == base->dtype && v.M == base->M && v.R * v.NT >= n && v.smem(T) <= kMaxSmem)
+      if (!best || score(&v) < score(best)) best = &v;
+  return best;
+}
+
 }  // namespace
 
 struct nsw_solver {
@@ -78,9 +90,11 @@ struct nsw_solver {
   int U = 0, n = 0, m = 0, T = 0, outer_max = 0, world = 1;
   nsw_solver_config cfg{};
   nsw_device_options opt{};
-  const Variant* var = nullptr;
+  const Variant* var = nullptr;   // tile of the main launch (users [0, U1))
   size_t smem = 0;
-  int chunks = 1;
+  const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
+  size_t smem2 = 0;
+  int U1 = 0;                     // users in the main launch (U1 == U: no tail launch)
   // device state
   void *C = nullptr, *am = nullptr, *av = nullptr, *alpha = nullptr, *beta = nullptr, *hist = nullptr,
        *xbest = nullptr, *rel = nullptr, *expo = nullptr;
@@ -98,8 +112,8 @@ struct nsw_solver {
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
   int64_t launches = 0;
-  StepArgs<float> a32{};
-  StepArgs<double> a64{};
+  StepArgs<float> a32{}, b32{};   // main / tail launch arguments
+  StepArgs<double> a64{}, b64{};
   FinalizeArgs fin{};
   float* flush_buf = nullptr;
   size_t flush_n = 0;
@@ -177,15 +191,34 @@ nsw_status validate_config(const nsw_solver_config* c) {
   return NSW_OK;
 }
 
-nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
+// The fused step over all users: the main launch covers users [0, U1) with
+// the occupancy-oriented tile; a tail of at most one user per SM (what is
+// left after whole waves) runs as a second launch with the wide tile, which
+// finishes a lone user several times faster.
+nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   void* args32[] = {&s->a32};
   void* args64[] = {&s->a64};
-  CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
-                            s->smem, st));
+  if (s->U1 > 0)
+    CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U1), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
+                              s->smem, st));
+  if (s->U1 < s->U) {
+    void* brgs32[] = {&s->b32};
+    void* brgs64[] = {&s->b64};
+    CUDA_TRY(cudaLaunchKernel(s->var2->fn, dim3(s->U - s->U1), dim3(s->var2->NT),
+                              s->dtype == NSW_F64 ? brgs64 : brgs32, s->smem2, st));
+    s->launches += 1;
+  }
+  s->launches += 1;
+  return NSW_OK;
+}
+
+nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
+  nsw_status e = launch_fused(s, st);
+  if (e != NSW_OK) return e;
   impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n,
                                                                                   s->imp_local, s->state);
   CUDA_TRY(cudaGetLastError());
-  s->launches += 2;
+  s->launches += 1;
   return NSW_OK;
 }
 
@@ -199,6 +232,9 @@ nsw_status launch_finalize(nsw_solver* s, cudaStream_t st) {
 nsw_status refresh_args(nsw_solver* s) {
   fill_step_args(s, s->a32);
   fill_step_args(s, s->a64);
+  s->b32 = s->a32;
+  s->b64 = s->a64;
+  s->b32.user0 = s->b64.user0 = s->U1;
   s->fin.n = s->n;
   s->fin.world = s->world;
   s->fin.outer_max = s->outer_max;
@@ -320,6 +356,33 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) != cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");
+  }
+  // Wave split: whole waves of the main tile, then (if what is left is at
+  // most one user per SM) a tail launch with the wide tile.
+  s->U1 = users_local;
+  if (options->variant < 0) {
+    int sms = 148, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);
+    const Variant* wide = choose_wide_variant(var, n, T);
+    const int slots = per_sm * sms;
+    if (wide && wide != var && slots > 0) {
+      const int rem = users_local % slots;
+      if (users_local <= sms) {
+        s->U1 = 0;  // at most one user per SM: all users on the wide tile
+      } else if (users_local > slots && rem > 0 && rem <= sms) {
+        s->U1 = users_local - rem;
+      }
+    }
+    if (s->U1 < users_local) {
+      s->var2 = wide;
+      s->smem2 = wide->smem(T);
+      if (cudaFuncSetAttribute(wide->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem2)) !=
+          cudaSuccess) {
+        nsw_solver_destroy(s);
+        return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem, tail) failed");
+      }
+    }
   }
   // inputs
   if ((e = s->dtype == NSW_F64 ? upload_converted<double>(s->rel, relevance_local, size_t(users_local) * n)
@@ -588,12 +651,16 @@ int64_t nsw_solver_launch_count(nsw_solver* s) { return s ? s->launches : -1; }
 
 nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT, int32_t* smem) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  // main tile; when a tail launch exists its shape is reported in the upper
+  // 16 bits of R and NT (R | R2 << 16, NT | NT2 << 16) and *smem is the main one
   if (M) *M = s->var->M;
-  if (R) *R = s->var->R;
-  if (NT) *NT = s->var->NT;
+  if (R) *R = s->var->R | (s->var2 && s->U1 < s->U ? s->var2->R << 16 : 0);
+  if (NT) *NT = s->var->NT | (s->var2 && s->U1 < s->U ? s->var2->NT << 16 : 0);
   if (smem) *smem = int(s->smem);
   return NSW_OK;
 }
+
+int32_t nsw_solver_tail_users(nsw_solver* s) { return s ? s->U - s->U1 : -1; }
 
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused) {
@@ -612,17 +679,15 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
       CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaEventRecord(ev[3 * i], s->stream));
-    void* args32[] = {&s->a32};
-    void* args64[] = {&s->a64};
-    CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U), dim3(s->var->NT),
-                              s->dtype == NSW_F64 ? args64 : args32, s->smem, s->stream));
+    nsw_status e = launch_fused(s, s->stream);
+    if (e != NSW_OK) return e;
     CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
     impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, s->stream>>>(
         s->partial, s->U, s->n, s->imp_local, s->state);
     finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));
-    s->launches += 3;
+    s->launches += 2;
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   float tot = 0.f, fus = 0.f;

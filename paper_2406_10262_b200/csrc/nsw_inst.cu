@@ -53,6 +53,8 @@ NSW_REG(8, 64, 6)
 NSW_REG(4, 128, 3)
 NSW_REG(8, 128, 3)
 NSW_REG(8, 256, 1)
+NSW_REG(2, 256, 1)
+NSW_REG(1, 512, 1)
 #elif NSW_M <= 16
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
@@ -61,12 +63,16 @@ NSW_REG(8, 64, 4)
 NSW_REG(4, 128, 2)
 NSW_REG(8, 128, 2)
 NSW_REG(8, 256, 1)
+NSW_REG(2, 256, 1)
+NSW_REG(1, 512, 1)
 #elif NSW_M <= 24
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 4)
 NSW_REG(4, 128, 1)
 NSW_REG(4, 256, 1)
+NSW_REG(2, 256, 1)
+NSW_REG(2, 512, 1)
 #else
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)

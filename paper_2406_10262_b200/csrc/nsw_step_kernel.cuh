@@ -19,6 +19,7 @@ namespace nsw {
 template <typename S>
 struct StepArgs {
   int U, n, m, T, outer_max, warm_start;
+  int user0;     // first user of this launch (the tail launch uses another tile)
   S* C;          // [U][n][m] transport costs (the ascent variable)
   S* am;         // [U][n][m] Adam first moment
   S* av;         // [U][n][m] Adam second moment
@@ -140,7 +141,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) return;
 
-  const int u = blockIdx.x;
+  const int u = a.user0 + blockIdx.x;
   const int tid = threadIdx.x;
   const int n = a.n, m = a.m;
   const int nm = n * m;
@@ -215,13 +216,13 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     __syncthreads();
     if (vec_ok) {
       const int nq = nm / V;
-      for (int q0 = tid; q0 < nq; q0 += 4 * NT) {
-        V16<S> c[4];
+      for (int q0 = tid; q0 < nq; q0 += 8 * NT) {
+        V16<S> c[8];
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < 8; ++b)
           if (q0 + b * NT < nq) c[b].v = reinterpret_cast<const V16<S>*>(Cu)[q0 + b * NT].v;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < 8; ++b) {
           const int q = q0 + b * NT;
           if (q >= nq) break;
           int i = q * V / m, k = q * V - i * m;

@@ -210,7 +210,11 @@ class DeviceSolver:
     def variant(self):
         M, R, NT, sm = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
         check(self.lib.nsw_solver_variant(self.h, C.byref(M), C.byref(R), C.byref(NT), C.byref(sm)))
-        return dict(M=M.value, R=R.value, NT=NT.value, smem=sm.value)
+        out = dict(M=M.value, R=R.value & 0xFFFF, NT=NT.value & 0xFFFF, smem=sm.value)
+        tail = int(self.lib.nsw_solver_tail_users(self.h))
+        if tail > 0:
+            out.update(tail_users=tail, tail_R=R.value >> 16, tail_NT=NT.value >> 16)
+        return out
 
     def launch_count(self) -> int:
         return int(self.lib.nsw_solver_launch_count(self.h))
