@@ -32,17 +32,20 @@ size_t smem_of(int T) {
                                             &smem_of<R, NT>});
 
 #if NSW_F64
+// parity instantiation: shapes up to 2048 (M <= 16) / 1024 (M <= 32) items
 #if NSW_M <= 16
 NSW_REG(1, 64, 1)
 NSW_REG(1, 128, 1)
 NSW_REG(1, 256, 1)
 NSW_REG(2, 256, 1)
 NSW_REG(2, 512, 1)
+NSW_REG(4, 512, 1)
 #else
 NSW_REG(1, 64, 1)
 NSW_REG(1, 128, 1)
 NSW_REG(1, 256, 1)
 NSW_REG(1, 512, 1)
+NSW_REG(2, 512, 1)
 #endif
 #else
 #if NSW_M <= 11

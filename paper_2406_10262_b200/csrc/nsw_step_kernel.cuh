@@ -201,16 +201,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
     for (int i = tid; i < n; i += NT) slotA(i) = a.alpha[size_t(u) * n + i];
-    for (int idx0 = tid; idx0 < (T + 1) * P; idx0 += 4 * NT) {
-      S hv[4];
+    for (int idx0 = tid; idx0 < (T + 1) * P; idx0 += 8 * NT) {
+      S hv[8];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < 8; ++j) {
         const int idx = idx0 + j * NT;
         const int t = idx / P, k = idx - t * P;
         hv[j] = (idx < (T + 1) * P && k < m) ? hu[size_t(t) * m + k] : S(0);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 8; ++j)
         if (idx0 + j * NT < (T + 1) * P) vh[idx0 + j * NT] = hv[j];
     }
     __syncthreads();
@@ -406,10 +406,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     };
     if (vec_ok) {
       const int nq = nm / V;
-      for (int q0 = tid; q0 < nq; q0 += 2 * NT) {
-        V16<S> c[2], mm[2], vv[2];
+      for (int q0 = tid; q0 < nq; q0 += 6 * NT) {
+        V16<S> c[6], mm[6], vv[6];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 6; ++b) {
           const int q = q0 + b * NT;
           if (q < nq) {
             c[b].v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           }
         }
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < 6; ++b) {
           const int q = q0 + b * NT;
           if (q >= nq) break;
           int i = q * V / m, k = q * V - i * m;
