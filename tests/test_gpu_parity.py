@@ -170,3 +170,34 @@ def test_full_cfg1_fp32_properties():
     assert np.abs(col[:, m - 1] - (x.shape[1] - m + 1)).max() / (x.shape[1] - m + 1) < 2e-4
     assert tr.objective[-1] > tr.objective[0]
     assert np.all(np.isfinite(tr.objective))
+
+
+@pytest.mark.parametrize("name,users,T,outer", [("cfg2", 3, 30, 3), ("cfg3", 2, 20, 3)])
+def test_baseline_shapes_fp64_vs_oracle(name, users, T, outer):
+    """BASELINE config-2 (1000 x 21, eps 0.02) and config-3 (2000 x 11, sparse
+    Zipf relevance) shapes on a user slice, float64 end to end vs the oracle."""
+    from paper_2406_10262_b200.data import make_instance
+    rel, expo, cfg = make_instance(name, seed=0, user_slice=(0, users))
+    p = orc.SolverParams(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    xd, trd = _solve(rel, expo, cfg.epsilon, T, outer, F64)
+    dx = np.abs(xd - xo).max()
+    df = np.abs(np.array(trd.objective) / np.array(tro.objective) - 1).max()
+    print(f"{name} slice fp64: |dX|={dx:.3e} rel dF={df:.3e}")
+    assert dx <= 1e-9 and df <= 1e-12
+
+
+@pytest.mark.parametrize("name,users,T", [("cfg2", 4, 40), ("cfg3", 3, 50)])
+def test_baseline_shapes_fp32_one_step(name, users, T):
+    """fp32 one-step parity at the config-2/3 shapes from the oracle's state at step 3."""
+    from paper_2406_10262_b200.data import make_instance
+    rel, expo, cfg = make_instance(name, seed=0, user_slice=(0, users))
+    p = orc.SolverParams(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=5, grad_threshold=1e-300)
+    _, _, states = orc.solve(rel, expo, p, record_states={3})
+    st = states[3]
+    ref = orc.one_step(rel, expo, st, p)
+    dev = _resume_step(rel, expo, p, st, 3, F32)
+    dx = np.abs(dev["plan"] - ref["plan"]).max()
+    dc = np.abs(dev["cost"] - ref["cost"]).max()
+    print(f"{name} one-step fp32: |dX|={dx:.3e} |dC|={dc:.3e}")
+    assert dx <= 5e-5 and dc <= 1e-4
