@@ -243,7 +243,7 @@ def run_ours(a):
     cfg = BASELINE_CONFIGS[a.config]
     rel, expo, _ = make_instance(a.config, seed=0, num_users=a.users)
     U, n, m, T = rel.shape[0], cfg.num_items, cfg.num_positions, a.inner or cfg.inner_iters
-    opts = DeviceOptions(dtype=a.dtype, device=local, variant=a.variant)
+    opts = DeviceOptions(dtype=a.dtype, schedule="fixed", device=local, variant=a.variant)
     scfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=a.warmup + a.steps + 2,
                         grad_threshold=1e-300)
     peaks, peaks_kind = _peaks()

@@ -67,6 +67,7 @@ typedef struct {
   int32_t variant;        /* -1 = automatic tile choice, else index into the table  */
   int32_t use_graph;      /* capture the outer step in a CUDA graph (1) or not (0)  */
   int32_t check_every;    /* host polls the stop flag every N outer steps           */
+  int32_t tol_chunk;      /* tolerance schedule: inner iterations per forward chunk */
 } nsw_device_options;
 
 /* Returned trace; mirrors SolveTrace (reference solver.py:125-135). */

@@ -104,6 +104,9 @@ struct nsw_solver {
   unsigned long long* stamp = nullptr;
   unsigned int* counter = nullptr;
   int* state = nullptr;
+  double* res = nullptr;   // tolerance mode: [U][T+1] residuals
+  int* iters = nullptr;    // [outer_max] inner iterations per step
+  int tol = 0;             // tolerance-mode schedule
   int* state_host = nullptr;  // pinned
   bool own_exchange = true;
   double* own_imp_local = nullptr;
@@ -143,6 +146,9 @@ void fill_step_args(nsw_solver* s, StepArgs<S>& a) {
   a.imp = s->imp_cur;
   a.state = s->state;
   a.bc = s->bc;
+  a.tol_mode = s->tol;
+  a.chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
+  a.res = s->res;
   const double eps = s->cfg.epsilon;
   a.nie = S(-1.0 / eps);
   a.lr = S(s->cfg.adam_lr);
@@ -216,7 +222,7 @@ nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
   nsw_status e = launch_fused(s, st);
   if (e != NSW_OK) return e;
   impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n,
-                                                                                  s->imp_local, s->state);
+                                                                                  s->imp_local, s->state, s->tol);
   CUDA_TRY(cudaGetLastError());
   s->launches += 1;
   return NSW_OK;
@@ -247,12 +253,18 @@ nsw_status refresh_args(nsw_solver* s) {
   s->fin.grad_norm = s->grad_norm;
   s->fin.stamp = s->stamp;
   s->fin.state = s->state;
+  s->fin.tol_mode = s->tol;
+  s->fin.U = s->U;
+  s->fin.T = s->T;
+  s->fin.tol = s->cfg.sinkhorn_tol;
+  s->fin.res = s->res;
+  s->fin.iters = s->iters;
   s->graph_dirty = true;
   return NSW_OK;
 }
 
 nsw_status read_state(nsw_solver* s) {
-  CUDA_TRY(cudaMemcpyAsync(s->state_host, s->state, 4 * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
+  CUDA_TRY(cudaMemcpyAsync(s->state_host, s->state, ST_WORDS * sizeof(int), cudaMemcpyDeviceToHost, s->stream));
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   return NSW_OK;
 }
@@ -287,8 +299,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     return fail(NSW_ERR_SHAPE, "need users > 0 and 2 <= num_positions <= num_items");
   if (world < 1) return fail(NSW_ERR_ARG, "world must be >= 1");
   if (options->dtype != NSW_F32 && options->dtype != NSW_F64) return fail(NSW_ERR_ARG, "bad dtype");
-  if (options->schedule != NSW_SCHEDULE_FIXED)
-    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is not implemented on the device yet");
+  if (options->schedule != NSW_SCHEDULE_FIXED && options->schedule != NSW_SCHEDULE_TOLERANCE)
+    return fail(NSW_ERR_ARG, "bad schedule");
+  if (options->schedule == NSW_SCHEDULE_TOLERANCE && world != 1)
+    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is single-GPU only (the lock-step test is not exchanged)");
   const int T = config->sinkhorn_max_iters;
   const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
   if (!var)
@@ -341,11 +355,14 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->bc, size_t(2) * (s->outer_max + 1) * 8);
   ALLOC(s->stamp, size_t(s->outer_max + 1) * 8);
   ALLOC(s->counter, 16);
-  ALLOC(s->state, 16);
+  ALLOC(s->state, ST_WORDS * sizeof(int));
+  ALLOC(s->iters, size_t(s->outer_max) * sizeof(int));
+  s->tol = options->schedule == NSW_SCHEDULE_TOLERANCE;
+  if (s->tol) ALLOC(s->res, size_t(users_local) * (T + 1) * 8);
 #undef ALLOC
   s->imp_local = s->own_imp_local;
   s->imp_all = world == 1 ? s->own_imp_local : s->own_imp_all;
-  if (cudaMallocHost((void**)&s->state_host, 16) != cudaSuccess) {
+  if (cudaMallocHost((void**)&s->state_host, ST_WORDS * sizeof(int)) != cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaMallocHost failed");
   }
@@ -417,7 +434,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     bc[2 * st2 + 1] = 1.0 - std::pow(config->adam_beta2, double(st2));
   }
   const double neg_inf = -INFINITY;
-  int init_state[4] = {PHASE_INIT, 0, 0, 0};
+  int init_state[ST_WORDS] = {PHASE_INIT, 0, 0, 0, 0, 0, 0, 0};
   if (cudaMemcpy(s->expo_d, ex.data(), m * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(s->rel_sq, rsq.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(s->bc, bc.data(), bc.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -443,7 +460,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
-                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf};
+                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (s->state_host) cudaFreeHost(s->state_host);
@@ -498,7 +515,36 @@ static nsw_status ensure_graph(nsw_solver* s) {
   return NSW_OK;
 }
 
+// Tolerance mode: the forward of a step runs in chunks until the lock-step
+// test (tol_check_kernel) finds t*; the host reads the device phase after
+// each chunk (the number of chunks is data dependent), then the finish
+// launch emits X^{t*}'s impact terms.
+static nsw_status one_step_tolerance(nsw_solver* s) {
+  nsw_status e = launch_fused(s, s->stream);
+  if (e != NSW_OK) return e;
+  const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
+  for (;;) {
+    tol_check_kernel<<<1, 256, 0, s->stream>>>(s->res, s->U, s->T, chunk, s->cfg.sinkhorn_tol, s->state);
+    CUDA_TRY(cudaGetLastError());
+    s->launches += 1;
+    e = read_state(s);
+    if (e != NSW_OK) return e;
+    const int ph = s->state_host[ST_PHASE];
+    if (ph == PHASE_FWD_CONT) {
+      e = launch_fused(s, s->stream);
+      if (e != NSW_OK) return e;
+      continue;
+    }
+    if (ph == PHASE_FWD_FIN) {
+      e = launch_step(s, s->stream);  // finish launch + impact reduction
+      if (e != NSW_OK) return e;
+    }
+    return launch_finalize(s, s->stream);
+  }
+}
+
 static nsw_status one_step(nsw_solver* s) {
+  if (s->tol) return one_step_tolerance(s);
   if (s->opt.use_graph) {
     nsw_status e = ensure_graph(s);
     if (e != NSW_OK) return e;
@@ -566,11 +612,19 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
       CUDA_TRY(cudaMemcpy(st.data(), s->stamp, (steps + 1) * 8, cudaMemcpyDeviceToHost));
     }
     for (int k = 0; k < steps; ++k) {
-      if (trace->sinkhorn_iterations) trace->sinkhorn_iterations[k] = s->T;
       if (trace->wall_time) trace->wall_time[k] = double(st[k + 1] - st[k]) * 1e-9;
     }
   }
+  if (trace && trace->sinkhorn_iterations && steps > 0)
+    CUDA_TRY(cudaMemcpy(trace->sinkhorn_iterations, s->iters, steps * sizeof(int), cudaMemcpyDeviceToHost));
   const int err = s->state_host[ST_ERR];
+  if (err & ERR_SOLVER) {
+    const double failed = 1.0 - double(s->state_host[ST_CONV]) / double(s->U);
+    char msg[160];
+    snprintf(msg, sizeof(msg), "Sinkhorn failed to converge for %.0f%% of users within %d iterations", failed * 100.0,
+             s->T);
+    return fail(NSW_ERR_SOLVER, msg);
+  }
   if (err & ERR_IMPACT) return fail(NSW_ERR_DOMAIN, "item impact became nonpositive during the solve");
   return NSW_OK;
 }
@@ -683,7 +737,7 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
     if (e != NSW_OK) return e;
     CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
     impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, s->stream>>>(
-        s->partial, s->U, s->n, s->imp_local, s->state);
+        s->partial, s->U, s->n, s->imp_local, s->state, s->tol);
     finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));

@@ -1,19 +1,26 @@
-// Cross-user pieces of one outer step: the impact reduction (solver.py:206)
-// and the scalar epilogue (objective, gradient norm, best iterate, stopping
-// rule; solver.py:207-223).  Both are latency kernels; they are ordered on
-// the solver's stream right after the fused per-user step kernel.
+// Cross-user pieces of one outer step: the impact reduction (solver.py:206),
+// the tolerance-mode stopping test (sinkhorn.py:244) and the scalar epilogue
+// (objective, gradient norm, best iterate, stopping rule; solver.py:200-223).
+// All are latency kernels ordered on the solver's stream after the fused
+// per-user step kernel.
 #include "nsw_step_kernel.cuh"
 
 namespace nsw {
+
+// The forward whose impact terms are ready: the fused launch in the fixed
+// schedule, the finish launch (PHASE_FWD_FIN) in tolerance mode.
+__device__ __forceinline__ bool forward_ready(int phase, int tol_mode) {
+  return tol_mode ? phase == PHASE_FWD_FIN
+                  : (phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME);
+}
 
 // One CTA per IMP_ITEMS consecutive items; its 256 threads stride over the
 // users (thread t: item t % IMP_ITEMS, user lane t / IMP_ITEMS), then a fixed
 // shared-memory tree combines the lanes: one pass, deterministic order.
 __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double* __restrict__ partial, int U,
                                                                     int n, double* __restrict__ imp_local,
-                                                                    const int* __restrict__ state) {
-  const int phase = state[ST_PHASE];
-  if (phase != PHASE_INIT && phase != PHASE_RUNNING && phase != PHASE_RESUME) return;
+                                                                    const int* __restrict__ state, int tol_mode) {
+  if (!forward_ready(state[ST_PHASE], tol_mode)) return;
   constexpr int LANES = IMP_THREADS / IMP_ITEMS;
   __shared__ double red[IMP_THREADS];
   const int j = threadIdx.x % IMP_ITEMS;
@@ -39,11 +46,47 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
   if (l == 0 && i < n) imp_local[i] = red[threadIdx.x];
 }
 
+__global__ void __launch_bounds__(256) tol_check_kernel(const double* __restrict__ res, int U, int T, int chunk,
+                                                        double tol, int* state) {
+  const int phase = state[ST_PHASE];
+  if (!(phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME || phase == PHASE_FWD_CONT)) return;
+  __shared__ double red[256];
+  __shared__ int tstar;
+  const int t0 = state[ST_T0];
+  const int t1 = min(t0 + chunk, T);
+  if (threadIdx.x == 0) tstar = 0;
+  for (int t = t0 + 1; t <= t1; ++t) {
+    double mx = 0.0;
+    for (int u = threadIdx.x; u < U; u += blockDim.x) mx = fmax(mx, res[size_t(u) * (T + 1) + t]);
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+      if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
+      __syncthreads();
+    }
+    const bool stop = red[0] <= tol;   // residual.max() <= tol (sinkhorn.py:244)
+    __syncthreads();
+    if (stop) {
+      if (threadIdx.x == 0) tstar = t;
+      break;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (tstar > 0 || t1 == T) {
+    state[ST_TSTAR] = tstar > 0 ? tstar : T;
+    state[ST_PHASE] = PHASE_FWD_FIN;
+  } else {
+    state[ST_T0] = t1;
+    state[ST_PHASE] = PHASE_FWD_CONT;
+  }
+}
+
 __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
   constexpr int NT = 512;
   __shared__ double sF[NT];
   __shared__ double sG[NT];
-  __shared__ int sBad;
+  __shared__ int sBad, sConv;
   const int tid = threadIdx.x;
   const int phase = f.state[ST_PHASE];
   if (phase == PHASE_FINISHED) return;
@@ -51,8 +94,19 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
     if (tid == 0) f.state[ST_PHASE] = PHASE_FINISHED;
     return;
   }
-  if (tid == 0) sBad = 0;
+  if (!forward_ready(phase, f.tol_mode)) return;
+  if (tid == 0) {
+    sBad = 0;
+    sConv = 0;
+  }
   __syncthreads();
+  const int tstar = f.tol_mode ? f.state[ST_TSTAR] : f.T;
+  if (f.tol_mode) {
+    // converged = residual <= tol at the final iteration (sinkhorn.py:253)
+    int cnt = 0;
+    for (int u = tid; u < f.U; u += NT) cnt += f.res[size_t(u) * (f.T + 1) + tstar] <= f.tol;
+    atomicAdd(&sConv, cnt);
+  }
   double accF = 0.0, accG = 0.0;
   int bad = 0;
   for (int i = tid; i < f.n; i += NT) {
@@ -76,6 +130,17 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
   }
   if (tid != 0) return;
   const int k = f.state[ST_STEP];
+  if (f.tol_mode) {
+    f.state[ST_CONV] = sConv;
+    f.state[ST_T0] = 0;
+    // SolverError if more than half the users missed the tolerance
+    // (solver.py:200-205), checked before the impact (solver.py:206-208)
+    if (1.0 - double(sConv) / double(f.U) > 0.5) {
+      f.state[ST_ERR] |= ERR_SOLVER;
+      f.state[ST_PHASE] = PHASE_FINISHED;
+      return;
+    }
+  }
   if (sBad) {  // DomainError (solver.py:207-208): stop before recording the step
     f.state[ST_ERR] |= ERR_IMPACT;
     f.state[ST_PHASE] = PHASE_FINISHED;
@@ -85,6 +150,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
   const double gn = sqrt(sG[0]);
   f.objective[k] = F;
   f.grad_norm[k] = gn;
+  f.iters[k] = tstar;
   f.stamp[k + 1] = globaltimer_ns();
   const int improved = F >= *f.best;  // ties go to the later step (solver.py:217)
   if (improved) *f.best = F;

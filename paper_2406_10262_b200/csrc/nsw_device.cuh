@@ -29,9 +29,24 @@ namespace nsw {
 // PHASE_RESUME: forward of step k from a caller-provided cost tensor, with the
 // warm-start duals lvi supplied in the `beta` buffer (checkpoint / resume,
 // and one-step parity from an oracle state).
-enum : int { PHASE_INIT = 0, PHASE_RUNNING = 1, PHASE_DONE_PENDING = 2, PHASE_FINISHED = 3, PHASE_RESUME = 4 };
-enum : int { ST_PHASE = 0, ST_STEP = 1, ST_IMPROVED = 2, ST_ERR = 3 };
-enum : int { ERR_IMPACT = 1, ERR_NONFINITE = 2 };
+// Tolerance mode (the reference's default stopping rule, sinkhorn.py:237-246)
+// runs each forward in chunks: PHASE_FWD_CONT = continue this step's forward,
+// PHASE_FWD_FIN = the lock-step stop t* is known, emit X^{t*}'s impact terms.
+enum : int {
+  PHASE_INIT = 0,
+  PHASE_RUNNING = 1,
+  PHASE_DONE_PENDING = 2,
+  PHASE_FINISHED = 3,
+  PHASE_RESUME = 4,
+  PHASE_FWD_CONT = 5,
+  PHASE_FWD_FIN = 6
+};
+// ST_T0: inner iterations done in the current forward; ST_TSTAR: iterations of
+// the last finished forward (the next backward's depth); ST_CONV: users within
+// tolerance at t* (for the > 50 % guard of solver.py:200-205).
+enum : int { ST_PHASE = 0, ST_STEP = 1, ST_IMPROVED = 2, ST_ERR = 3, ST_T0 = 4, ST_TSTAR = 5, ST_CONV = 6 };
+constexpr int ST_WORDS = 8;
+enum : int { ERR_IMPACT = 1, ERR_NONFINITE = 2, ERR_SOLVER = 4 };
 
 template <typename S>
 struct Fp;

@@ -20,6 +20,9 @@ template <typename S>
 struct StepArgs {
   int U, n, m, T, outer_max, warm_start;
   int user0;     // first user of this launch (the tail launch uses another tile)
+  int tol_mode;  // 0: fixed schedule; 1: reference tolerance mode (chunked forward)
+  int chunk;     // tolerance mode: inner iterations per forward launch
+  double* res;   // tolerance mode: [U][T+1] L-inf marginal residual after iteration t
   S* C;          // [U][n][m] transport costs (the ascent variable)
   S* am;         // [U][n][m] Adam first moment
   S* av;         // [U][n][m] Adam second moment
@@ -87,7 +90,8 @@ template <typename S, int M, int R, int NT>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
-  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows);
+  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
+                      size_t(NT / 32) + 2);
 }
 
 // fp32 throughput path: divisions / square roots off the hot path use the
@@ -132,7 +136,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* vec1 = vec0 + P;                       // [P] beta / column max
   S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
   S* rowA = vec2 + P;                       // [NT*R] (no padding column only)
-  S* rowB = rowA + size_t(NT) * R;
+  S* rowB = rowA + (PAD ? 0 : size_t(NT) * R);
+  S* colres = rowB + (PAD ? 0 : size_t(NT) * R);  // [2][P] column residuals (tolerance mode)
+  S* redmax = colres + 2 * P;                     // [NW] per-warp row-residual maxima
   // slotA: alpha -> u~^T -> u^1 ; slotB: seed g_u (shares slotA's storage
   // when PAD: written after u~^T is in registers, u~^T restored at level T)
   auto slotA = [&](int i) -> S& { return PAD ? Kt[size_t(i) * P + M] : rowA[i]; };
@@ -140,6 +146,13 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) return;
+  const bool tolm = a.tol_mode != 0;
+  // Length of the v~ history of the K~ this launch rebuilds: the previous
+  // solve's iteration count for the backward / owed policy, the iterations
+  // done so far for a forward continuation, the stopping iteration t* for
+  // the forward's finish (tolerance mode; the fixed schedule always has T).
+  const int Tprev = tolm ? a.state[ST_TSTAR] : T;
+  const int Th = phase == PHASE_FWD_CONT ? a.state[ST_T0] : (phase == PHASE_FWD_FIN ? a.state[ST_TSTAR] : Tprev);
 
   const int u = a.user0 + blockIdx.x;
   const int tid = threadIdx.x;
@@ -197,21 +210,22 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
   __syncthreads();
 
-  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
-    // ---------------- rebuild K~ of step k-1 from C, alpha, beta ------------
+  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING || phase == PHASE_FWD_CONT || phase == PHASE_FWD_FIN) {
+    // ---------------- rebuild K~ from C, alpha, beta (step k-1's for the
+    // backward; this step's for a tolerance-mode continuation / finish) ------
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
     for (int i = tid; i < n; i += NT) slotA(i) = a.alpha[size_t(u) * n + i];
-    for (int idx0 = tid; idx0 < (T + 1) * P; idx0 += 8 * NT) {
+    for (int idx0 = tid; idx0 < (Th + 1) * P; idx0 += 8 * NT) {
       S hv[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const int idx = idx0 + j * NT;
         const int t = idx / P, k = idx - t * P;
-        hv[j] = (idx < (T + 1) * P && k < m) ? hu[size_t(t) * m + k] : S(0);
+        hv[j] = (idx < (Th + 1) * P && k < m) ? hu[size_t(t) * m + k] : S(0);
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (idx0 + j * NT < (T + 1) * P) vh[idx0 + j * NT] = hv[j];
+        if (idx0 + j * NT < (Th + 1) * P) vh[idx0 + j * NT] = hv[j];
     }
     __syncthreads();
     if (vec_ok) {
@@ -241,10 +255,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     }
     __syncthreads();
     S vT[M];
-    lds_vec<S, M>(vT, vh + size_t(T) * P);
+    lds_vec<S, M>(vT, vh + size_t(Th) * P);
     {
       S vT1[M];
-      lds_vec<S, M>(vT1, vh + size_t(T - 1) * P);
+      lds_vec<S, M>(vT1, vh + size_t(Th - 1) * P);
 #pragma unroll 1
       for (int i = tid; i < NT * R; i += NT) {
         S kr[M];
@@ -261,12 +275,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           V16<S> t;
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            t.s[j] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(T) * P + k]);
+            t.s[j] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(Th) * P + k]);
             if (++k == m) { k = 0; ++i; }
           }
           reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
         } else {
-          xb[e0] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(T) * P + k]);
+          xb[e0] = mul_(mul_(Kt[i * P + k], slotA(i)), vh[size_t(Th) * P + k]);
         }
       }
     };
@@ -277,6 +291,28 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         write_policy();
       }
       return;
+    }
+    if (phase == PHASE_FWD_FIN) {
+      // tolerance mode: the forward stopped at t* = Th; impact terms of X^{t*}
+#pragma unroll 1
+      for (int i = tid; i < n; i += NT) {
+        S kr[M];
+        lds_vec<S, M>(kr, Kt + size_t(i) * P);
+        const S uT = slotA(i);
+        const double rr = double(relu[i]);
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k)
+          if (k < m - 1) acc = fma(rr * a.expo_d[(k < m - 1) ? k : 0], double(mul_(mul_(kr[k], uT), vT[k])), acc);
+        a.partial[size_t(u) * n + i] = acc;
+      }
+      return;
+    }
+    if (phase == PHASE_FWD_CONT) {
+      // tolerance mode: continue this step's forward from v~^{t0}, t0 = Th
+      if (tid < P) vec0[tid] = vh[size_t(Th) * P + tid];
+      __syncthreads();
+      goto forward_iterations;
     }
     __syncthreads();
     if (improved) write_policy();   // best-so-far policy is step k-1's (solver.py:217-219)
@@ -312,7 +348,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         slotB(i) = gsum;
       }
       cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-        vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
+        vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
       });
     }
 
@@ -322,12 +358,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
     //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
     //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 2)
-    for (int t = T; t >= 1; --t) {
+    for (int t = Th; t >= 1; --t) {
       S cv[M], vp[M], c[M];
       lds_vec<S, M>(cv, vec0);
       lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
       const S* vppp = vh + size_t(t >= 2 ? t - 2 : 0) * P;
-      const bool first = t == T;
+      const bool first = t == Th;
       const bool replay = t >= 2;
 #pragma unroll
       for (int k = 0; k < M; ++k) c[k] = S(0);
@@ -383,7 +419,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       }
       sts_vec<S, M>(Kt + size_t(i) * P, gk);
     }
-    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
     __syncthreads();
 
     // ---------------- g_C = gK * (-1/eps); Adam ascent  (solver.py:105-122) -
@@ -521,30 +557,84 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     }
   }
   __syncthreads();
-  S A[R][M];  // K~, register resident
-  S ut[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) lds_vec<S, M>(A[r], Kt + size_t(tid + r * NT) * P);
-  for (int t = 1; t <= T; ++t) {
-    S vv[M], c[M];
-    lds_vec<S, M>(vv, vec0);
+forward_iterations:
+  {
+    S A[R][M];  // K~, register resident
+    S ut[R];
+    const int t_start = phase == PHASE_FWD_CONT ? Th + 1 : 1;
+    const int t_end = tolm ? min(t_start - 1 + a.chunk, T) : T;
+    const int lane = tid & 31, warp = tid >> 5;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const S rp = F::rcp_fast(rdot<S, M>(A[r], vv));
-      ut[r] = ok(r) ? rp : S(0);
+      lds_vec<S, M>(A[r], Kt + size_t(tid + r * NT) * P);
+      ut[r] = S(0);
     }
+    // tolerance mode also records the reference's L-inf marginal residual of
+    // every iteration (sinkhorn.py:237-243): the row sums of X^{t-1} are
+    // u~^{t-1} (K~ v~^{t-1}) -- the next iteration's own row dot -- and the
+    // column sums are v~ times the column totals.
+    auto warp_max = [&](S x) {
 #pragma unroll
-    for (int k = 0; k < M; ++k) {
-      c[k] = A[0][k] * ut[0];
+      for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+      return x;
+    };
+    for (int t = t_start; t <= t_end; ++t) {
+      S vv[M], c[M];
+      lds_vec<S, M>(vv, vec0);
+      S rmax = S(0);
 #pragma unroll
-      for (int r = 1; r < R; ++r) c[k] = fma(A[r][k], ut[r], c[k]);
+      for (int r = 0; r < R; ++r) {
+        const S sr = rdot<S, M>(A[r], vv);
+        if (tolm && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
+        ut[r] = ok(r) ? F::rcp_fast(sr) : S(0);
+      }
+      if (tolm) {
+        rmax = warp_max(rmax);
+        if (lane == 0) redmax[warp] = rmax;
+      }
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        c[k] = A[0][k] * ut[0];
+#pragma unroll
+        for (int r = 1; r < R; ++r) c[k] = fma(A[r][k], ut[r], c[k]);
+      }
+      cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+        const S vn = F::div_fast(mass(k), tot);
+        vec0[k] = vn;
+        hu[size_t(t) * m + k] = vn;
+        if (tolm) {
+          // fp64: |v~ (K~' u~) - colmass| as the reference measures it; fp32
+          // cannot resolve 1e-6 against the dummy mass, and the columns are
+          // normalised exactly by construction, so it counts as 0 there.
+          colres[(t & 1) * P + k] = sizeof(S) == 8 ? fabs(vn * tot - mass(k)) : S(0);
+          if (k == 0 && t > t_start) {
+            S r = S(0);
+            for (int w = 0; w < NW; ++w) r = fmax(r, redmax[w]);
+            for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[((t - 1) & 1) * P + kk]);
+            a.res[size_t(u) * (T + 1) + t - 1] = double(r);
+          }
+        }
+      });
     }
-    cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-      const S vn = F::div_fast(mass(k), tot);
-      vec0[k] = vn;
-      hu[size_t(t) * m + k] = vn;
-    });
-  }
+    if (tolm) {
+      // residual of the chunk's last iteration needs one more row pass
+      S vv[M];
+      lds_vec<S, M>(vv, vec0);
+      S rmax = S(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M>(A[r], vv) - S(1)));
+      rmax = warp_max(rmax);
+      if (lane == 0) redmax[warp] = rmax;
+      __syncthreads();
+      if (tid == 0) {
+        S r = S(0);
+        for (int w = 0; w < NW; ++w) r = fmax(r, redmax[w]);
+        for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[(t_end & 1) * P + kk]);
+        a.res[size_t(u) * (T + 1) + t_end] = double(r);
+      }
+      return;  // impact terms come from the finish launch once t* is known
+    }
   // per-item impact terms of this user (solver.py:206), float64
   {
     S vv[M];
@@ -564,6 +654,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       if (ok(r)) a.partial[size_t(u) * n + i] = acc;
     }
   }
+  }
 }
 
 // --------------------------------------------------------------------------
@@ -573,7 +664,13 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 constexpr int IMP_THREADS = 256;
 constexpr int IMP_ITEMS = 8;
 __global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n,
-                                     double* __restrict__ imp_local, const int* __restrict__ state);
+                                     double* __restrict__ imp_local, const int* __restrict__ state, int tol_mode);
+
+// Tolerance mode: after each forward chunk, the lock-step stopping test of
+// sinkhorn.py:244 over all users: t* = first iteration whose max residual is
+// <= tol; sets PHASE_FWD_FIN (t* found or the budget is spent) or
+// PHASE_FWD_CONT (next chunk).
+__global__ void tol_check_kernel(const double* __restrict__ res, int U, int T, int chunk, double tol, int* state);
 
 struct FinalizeArgs {
   int n, world, outer_max;
@@ -587,6 +684,10 @@ struct FinalizeArgs {
   double* grad_norm;       // [outer_max]
   unsigned long long* stamp;  // [outer_max+1] globaltimer ns
   int* state;
+  int tol_mode, U, T;
+  double tol;
+  const double* res;       // [U][T+1] residuals (tolerance mode)
+  int* iters;              // [outer_max] inner iterations per step (trace)
 };
 
 __global__ void finalize_kernel(FinalizeArgs f);

@@ -62,7 +62,7 @@ class ShardedAscent:
         rsq_local = torch.tensor((rel[self.start:self.stop] ** 2).sum(axis=0), dtype=torch.float64, device=dev)
         dist.all_reduce(rsq_local, group=group)
         rsq = rsq_local.cpu().numpy()
-        opts = options or DeviceOptions()
+        opts = options or DeviceOptions(schedule="fixed")
         self.solver = DeviceSolver(rel[self.start:self.stop], exposure.values, shape.num_items,
                                    shape.num_positions, config, opts, rel_sq_sum=rsq, world=self.world)
         n = shape.num_items
@@ -117,7 +117,7 @@ def solve_fair_ranking_distributed(relevance, exposure, shape, config, options: 
     relevance, exposure, shape, config = _coerce(relevance, exposure, shape, config)
     _check_instance(relevance.values, exposure.values, shape)
     sa = ShardedAscent(relevance, exposure, shape, config, options, group)
-    done = sa.run(config.outer_max_iters + 1, use_graph=bool((options or DeviceOptions()).use_graph))
+    done = sa.run(config.outer_max_iters + 1, use_graph=bool((options or DeviceOptions(schedule="fixed")).use_graph))
     torch.cuda.synchronize()
     if not done:
         raise SolverError("distributed solve did not reach its stop state")

@@ -18,8 +18,8 @@ from paper_2406_10262_b200 import (DeviceOptions, DeviceSolver, ExposureModel, P
 
 pytestmark = pytest.mark.gpu
 
-F64 = DeviceOptions(dtype="float64")
-F32 = DeviceOptions(dtype="float32")
+F64 = DeviceOptions(dtype="float64", schedule="fixed")
+F32 = DeviceOptions(dtype="float32", schedule="fixed")
 
 
 def _solve(rel, expo, eps, inner, outer, opts, **kw):
@@ -96,7 +96,7 @@ def test_one_step_from_oracle_state(golden, dtype, tol_x, tol_c):
     _, _, states = orc.solve(rel, expo, p, record_states={10})
     st = states[10]
     ref = orc.one_step(rel, expo, st, p)
-    dev = _resume_step(rel, expo, p, st, 10, DeviceOptions(dtype=dtype))
+    dev = _resume_step(rel, expo, p, st, 10, DeviceOptions(dtype=dtype, schedule="fixed"))
     dx = np.abs(dev["plan"] - ref["plan"]).max()
     dc = np.abs(dev["cost"] - ref["cost"]).max()
     df = abs(dev["objective"] / st["objective"] - 1)
