@@ -30,7 +30,7 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
 # (f64?, M) instantiations of the fused step kernel; any m <= 32 pads up.
 INSTANCES = [(f64, M) for f64 in (0, 1) for M in (4, 8, 11, 16, 21, 32)]
 
-HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_registry.h", "nsw_ops.cuh"]
+HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_registry.h"]
 
 
 def _nvcc():
@@ -51,6 +51,9 @@ def _jobs():
         tag = f"inst_{'f64' if f64 else 'f32'}_M{M}"
         jobs.append((os.path.join(CSRC, "nsw_inst.cu"), os.path.join(BUILD, tag + ".o"),
                      [f"-DNSW_F64={f64}", f"-DNSW_M={M}"]))
+    for f64 in (0, 1):
+        jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(BUILD, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
+                     [f"-DNSW_F64={f64}"]))
     for name in ("nsw_common", "nsw_capi", "nsw_ops"):
         jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(BUILD, name + ".o"), []))
     return jobs

@@ -53,12 +53,17 @@ int sizeof_dtype(int dt) { return dt == NSW_F64 ? 8 : 4; }
 const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
   auto& reg = variant_registry();
   std::vector<const Variant*> c;
-  for (auto& v : reg)
-    if (v.dtype == dtype && v.M >= m && v.R * v.NT >= n && v.smem(T) <= kMaxSmem) c.push_back(&v);
+  // one-CTA-per-user tiles first; cluster tiles (CL > 1 CTAs per user) only
+  // when no single-CTA tile holds the user's n x m tile
+  for (int pass = 0; pass < 2 && c.empty(); ++pass)
+    for (auto& v : reg)
+      if (v.dtype == dtype && v.M >= m && v.CL * v.rows >= n && v.smem(T) <= kMaxSmem && (v.CL > 1) == (pass == 1))
+        c.push_back(&v);
   if (c.empty()) return nullptr;
   std::sort(c.begin(), c.end(), [](const Variant* a, const Variant* b) {
     if (a->M != b->M) return a->M < b->M;
-    if (a->R * a->NT != b->R * b->NT) return a->R * a->NT < b->R * b->NT;
+    if (a->CL != b->CL) return a->CL < b->CL;
+    if (a->rows != b->rows) return a->rows < b->rows;
     return a->R > b->R;
   });
   if (forced >= 0) {
@@ -78,7 +83,7 @@ const Variant* choose_wide_variant(const Variant* base, int n, int T) {
   const Variant* best = nullptr;
   auto score = [](const Variant* v) { return std::abs(v->R - 2) * 4096 + v->NT; };
   for (auto& v : variant_registry())
-    if (v.dtype == base->dtype && v.M == base->M && v.R * v.NT >= n && v.smem(T) <= kMaxSmem)
+    if (v.dtype == base->dtype && v.M == base->M && v.CL == 1 && v.rows >= n && v.smem(T) <= kMaxSmem)
       if (!best || score(&v) < score(best)) best = &v;
   return best;
 }
@@ -204,6 +209,24 @@ nsw_status validate_config(const nsw_solver_config* c) {
 nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   void* args32[] = {&s->a32};
   void* args64[] = {&s->a64};
+  if (s->var->CL > 1) {
+    // thread-block cluster of CL CTAs per user (DSMEM column reductions)
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(s->var->CL);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.gridDim = dim3(unsigned(s->U) * s->var->CL);
+    lc.blockDim = dim3(s->var->NT);
+    lc.dynamicSmemBytes = s->smem;
+    lc.stream = st;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelExC(&lc, s->var->fn, s->dtype == NSW_F64 ? args64 : args32));
+    s->launches += 1;
+    return NSW_OK;
+  }
   if (s->U1 > 0)
     CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U1), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
                               s->smem, st));
@@ -377,7 +400,11 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   // Wave split: whole waves of the main tile, then (if what is left is at
   // most one user per SM) a tail launch with the wide tile.
   s->U1 = users_local;
-  if (options->variant < 0) {
+  if (var->CL > 1 && options->schedule == NSW_SCHEDULE_TOLERANCE) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is not available for cluster tiles (m > 32 or large n)");
+  }
+  if (options->variant < 0 && var->CL == 1) {
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);

@@ -1,5 +1,5 @@
 // Registry of compiled fused-step tile variants (one entry per template
-// instantiation; filled by static initialisers in nsw_inst.cu).
+// instantiation; filled by static initialisers in nsw_inst*.cu).
 #pragma once
 #include <cstddef>
 #include <vector>
@@ -13,12 +13,17 @@ struct Variant {
   int NT;     // threads per CTA
   const void* fn;
   size_t (*smem)(int T);
+  int CL = 1;     // CTAs per user (thread-block cluster) ; 1 = one CTA per user
+  int rows = 0;   // items per CTA (R * NT for the 1-D tiles)
 };
 
 std::vector<Variant>& variant_registry();
 
 struct Registrar {
-  explicit Registrar(const Variant& v) { variant_registry().push_back(v); }
+  explicit Registrar(Variant v) {
+    if (v.rows == 0) v.rows = v.R * v.NT;
+    variant_registry().push_back(v);
+  }
 };
 
 }  // namespace nsw

@@ -1,0 +1,499 @@
+// Cluster tile of the fused outer step, for users whose n x m tile does not
+// fit one SM (BASELINE config 4: n = 4000, m = 51 -> 204k cells per user).
+//
+// A user is split over a thread-block cluster of CL CTAs (one per SM), each
+// owning NR = (NT / CG) * R consecutive items.  Inside a CTA the mapping is
+// two-dimensional: CG consecutive lanes share a row group and each owns MC of
+// the (padded) MC * CG columns, so every per-thread vector has MC entries --
+// a 1-D row-per-thread mapping would need 5 * 51 registers of vectors at
+// m = 51.  Row sums finish with a log2(CG)-step xor butterfly across the
+// group; column sums with a reduce-scatter over the row-group lanes, a
+// fixed-order cross-warp sum and a fixed-order sum of the CL CTA totals read
+// through distributed shared memory (every CTA computes the same bits).
+// Numerics are identical in form to step_kernel (nsw_step_kernel.cuh).
+// Fixed schedule only.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "nsw_step_kernel.cuh"
+
+namespace nsw {
+
+template <typename S, int MC, int CG, int R, int NT, int CL>
+struct ClTile {
+  static constexpr int MP = MC * CG;                                  // padded columns
+  static constexpr int P = (MC % 2) ? MP + 1 : Pitch<S, MP>::value;   // smem pitch
+  static constexpr int RG = NT / CG;                                  // row groups per CTA
+  static constexpr int NR = RG * R;                                   // items per CTA
+  static constexpr int NW = NT / 32;
+};
+
+template <typename S, int MC, int CG, int R, int NT, int CL>
+__host__ __device__ constexpr size_t cl_smem_bytes(int T) {
+  using Tl = ClTile<S, MC, CG, R, NT, CL>;
+  return sizeof(S) * (size_t(Tl::NR) * Tl::P + size_t(T + 1) * Tl::P + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
+                      2 * size_t(Tl::NR) + 2 * Tl::P + 4);
+}
+
+// Reduce-scatter across the row-group lanes (xor offsets 16 .. CG).
+template <typename S, int N, int CNT, int OFF, int CGM, class Op>
+__device__ __forceinline__ void rs_rows(S (&v)[N], int lane, int& base, int& lim) {
+  if constexpr (OFF >= CGM) {
+    constexpr int H = (CNT + 1) / 2;
+    const bool up = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      const S lo = v[j];
+      const S hi = (j + H < CNT) ? v[(j + H < CNT) ? (j + H) : 0] : Op::template identity<S>();
+      const S send = up ? lo : hi;
+      const S keep = up ? hi : lo;
+      v[j] = Op{}(keep, __shfl_xor_sync(0xffffffffu, send, OFF));
+    }
+    if (up) {
+      base += H;
+    } else {
+      lim = min(lim, base + H);
+    }
+    rs_rows<S, N, H, OFF / 2, CGM, Op>(v, lane, base, lim);
+  }
+}
+
+template <int CNT, int OFF, int CGM>
+__host__ __device__ constexpr int rs_final_count() {
+  if constexpr (OFF >= CGM) return rs_final_count<(CNT + 1) / 2, OFF / 2, CGM>();
+  else return CNT;
+}
+
+template <typename S, int CG>
+__device__ __forceinline__ S group_sum(S x) {
+#pragma unroll
+  for (int o = 1; o < CG; o <<= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+template <typename S, int CG>
+__device__ __forceinline__ S group_max(S x) {
+#pragma unroll
+  for (int o = 1; o < CG; o <<= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  return x;
+}
+
+// Row dot of this lane's MC-column segment, completed across the group.
+template <typename S, int MC, int CG>
+__device__ __forceinline__ S rdot_g(const S (&x)[MC], const S (&y)[MC]) {
+  return group_sum<S, CG>(rdot<S, MC>(x, y));
+}
+
+template <typename S, int MC>
+__device__ __forceinline__ void ld_seg(S (&dst)[MC], const S* src) {
+#pragma unroll
+  for (int j = 0; j < MC; ++j) dst[j] = src[j];
+}
+
+template <typename S, int MC>
+__device__ __forceinline__ void st_seg(S* dst, const S (&src)[MC]) {
+#pragma unroll
+  for (int j = 0; j < MC; ++j) dst[j] = src[j];
+}
+
+template <typename S, int MC, int CG, int R, int NT, int CL>
+__global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
+  using F = Fp<S>;
+  using Tl = ClTile<S, MC, CG, R, NT, CL>;
+  constexpr int P = Tl::P, RG = Tl::RG, NR = Tl::NR, NW = Tl::NW;
+  constexpr int V = 16 / sizeof(S);
+  static_assert(32 % CG == 0 && NT % 32 == 0, "tile shape");
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = a.T;
+  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][P]
+  S* vh = Kt + size_t(NR) * P;              // [T+1][P]
+  S* red = vh + size_t(T + 1) * P;          // [NW][P]
+  S* vec0 = red + NW * P;
+  S* vec1 = vec0 + P;
+  S* vec2 = vec1 + P;
+  S* rowA = vec2 + P;                       // [NR]
+  S* rowB = rowA + NR;                      // [NR]
+  S* clred = rowB + NR;                     // [2][P] this CTA's column totals
+
+  const int phase = a.state[ST_PHASE];
+  if (phase == PHASE_FINISHED) {
+    cluster.sync();
+    return;
+  }
+  const int rank = int(cluster.block_rank());
+  const int u = a.user0 + int(blockIdx.x) / CL;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = tid % CG, rg = tid / CG;
+  const int n = a.n, m = a.m;
+  const int r0 = rank * NR;                           // first item of this CTA
+  const int nloc = max(0, min(NR, n - r0));           // items of this CTA
+  const int ncell = nloc * m;
+  const size_t ubase = size_t(u) * n * m + size_t(r0) * m;
+  S* Cu = a.C + ubase;
+  S* mu = a.am + ubase;
+  S* vu = a.av + ubase;
+  S* xb = a.xbest + ubase;
+  S* hu = a.hist + size_t(u) * (T + 1) * m;
+  const S* relu = a.rel + size_t(u) * n + r0;
+  const bool vec_ok = (size_t(n) * m % V == 0) && (size_t(NR) * m % V == 0);
+  int parity = 0;
+  auto lrow = [&](int r) { return rg + r * RG; };
+  auto ok = [&](int r) { return lrow(r) < nloc; };
+  auto col = [&](int j) { return g * MC + j; };
+  auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
+  auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
+  auto ktilde = [&](S c, S beta_k, S alpha_i) -> S {
+    return F::exp_fast(add_(add_(mul_(c, a.nie), beta_k), alpha_i));
+  };
+  auto gx_of = [&](S rr, S e, S imp_i, S inv_imp) -> S {
+    if constexpr (sizeof(S) == 4) return mul_(mul_(rr, e), inv_imp);
+    else return F::div(mul_(rr, e), imp_i);
+  };
+  // column reduction over the whole cluster; fin(k, total) on thread k < m
+  // of every CTA (identical bits everywhere)
+  auto reduce_cols = [&](S (&v)[MC], auto&& fin) {
+    int base = 0, lim = MC;
+    rs_rows<S, MC, MC, 16, CG, OpSum>(v, lane, base, lim);
+    constexpr int CF = rs_final_count<MC, 16, CG>();
+#pragma unroll
+    for (int j = 0; j < CF; ++j) {
+      const int c = g * MC + base + j;
+      if (base + j < lim && c < m) red[warp * P + c] = v[j];
+    }
+    __syncthreads();
+    S acc = S(0);
+    if (tid < m) {
+      acc = red[tid];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) acc += red[w * P + tid];
+      if constexpr (CL > 1) clred[parity * P + tid] = acc;
+    }
+    if constexpr (CL > 1) {
+      cluster.sync();
+      if (tid < m) {
+        S tot = S(0);
+#pragma unroll
+        for (int q = 0; q < CL; ++q) tot += *cluster.map_shared_rank(clred + parity * P + tid, q);
+        fin(tid, tot);
+      }
+      parity ^= 1;
+    } else {
+      if (tid < m) fin(tid, acc);
+    }
+    __syncthreads();
+  };
+  // coalesced element-wise visit of this CTA's cells: f(local cell e, vector slot or -1)
+  auto foreach_cell = [&](auto&& f) {
+    if (vec_ok) {
+      for (int q = tid; q < ncell / V; q += NT) f(q * V, q);
+    } else {
+      for (int e = tid; e < ncell; e += NT) f(e, -1);
+    }
+  };
+
+  for (int q = tid; q < NR * P; q += NT) Kt[q] = S(0);
+  if (tid < P) {
+    vec0[tid] = S(0);
+    vec1[tid] = S(0);
+    vec2[tid] = S(0);
+    clred[tid] = S(0);
+    clred[P + tid] = S(0);
+  }
+  S ex[MC];
+#pragma unroll
+  for (int j = 0; j < MC; ++j) ex[j] = (col(j) < m - 1) ? a.expo[min(col(j), m - 2)] : S(0);
+  __syncthreads();
+
+  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
+    // ---- rebuild K~ of step k-1 (this CTA's items) ----
+    if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
+    for (int i = tid; i < nloc; i += NT) rowA[i] = a.alpha[size_t(u) * n + r0 + i];
+    for (int idx = tid; idx < (T + 1) * P; idx += NT) {
+      const int t = idx / P, k = idx - t * P;
+      vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
+    }
+    __syncthreads();
+    foreach_cell([&](int e0, int q) {
+      int i = e0 / m, k = e0 - i * m;
+      if (q >= 0) {
+        V16<S> c;
+        c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          Kt[i * P + k] = ktilde(c.s[j], vec1[k], rowA[i]);
+          if (++k == m) { k = 0; ++i; }
+        }
+      } else {
+        Kt[i * P + k] = ktilde(Cu[e0], vec1[k], rowA[i]);
+      }
+    });
+    __syncthreads();
+    S vT[MC];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) vT[j] = vh[size_t(T) * P + col(j)];
+    {
+      S vT1[MC];
+#pragma unroll
+      for (int j = 0; j < MC; ++j) vT1[j] = vh[size_t(T - 1) * P + col(j)];
+      for (int r = 0; r < R; ++r) {   // u~^T (all lanes of the group agree)
+        S kr[MC];
+        ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * P + g * MC);
+        const S uT = F::rcp_fast(rdot_g<S, MC, CG>(kr, vT1));
+        __syncwarp();
+        if (g == 0) rowA[lrow(r)] = ok(r) ? uT : S(0);
+      }
+    }
+    __syncthreads();
+    const int improved = a.state[ST_IMPROVED];
+    auto write_policy = [&]() {
+      foreach_cell([&](int e0, int q) {
+        int i = e0 / m, k = e0 - i * m;
+        if (q >= 0) {
+          V16<S> t;
+#pragma unroll
+          for (int j = 0; j < V; ++j) {
+            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+            if (++k == m) { k = 0; ++i; }
+          }
+          reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
+        } else {
+          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+        }
+      });
+    };
+    if (phase == PHASE_DONE_PENDING) {
+      if (improved) write_policy();
+      cluster.sync();
+      return;
+    }
+    if (improved) write_policy();
+
+    // ---- seed W = gx .* X, reverse sweep (see step_kernel) ----
+    S A[R][MC];
+    S ut[R];
+    {
+      S c[MC];
+#pragma unroll
+      for (int j = 0; j < MC; ++j) c[j] = S(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int il = lrow(r);
+        S kr[MC];
+        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        ut[r] = rowA[il];
+        const S rr = ok(r) ? relu[il] : S(0);
+        const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
+        const S inv_imp = S(1.0 / double(imp_i));
+        S gsum = S(0);
+#pragma unroll
+        for (int j = 0; j < MC; ++j) {
+          A[r][j] = S(0);
+          if (col(j) < m - 1) {
+            const S W = mul_(gx_of(rr, ex[j], imp_i, inv_imp), mul_(mul_(kr[j], ut[r]), vT[j]));
+            gsum += W;
+            c[j] += W;
+          }
+        }
+        gsum = group_sum<S, CG>(gsum);
+        if (g == 0) rowB[il] = gsum;
+      }
+      reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k)); });
+    }
+    for (int t = T; t >= 1; --t) {
+      S cv[MC], vp[MC], vpp[MC], c[MC];
+#pragma unroll
+      for (int j = 0; j < MC; ++j) {
+        cv[j] = vec0[col(j)];
+        vp[j] = vh[size_t(t - 1) * P + col(j)];
+        vpp[j] = vh[size_t(t >= 2 ? t - 2 : 0) * P + col(j)];
+        c[j] = S(0);
+      }
+      const bool first = t == T;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int il = lrow(r);
+        S kr[MC];
+        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        const S sig = rdot_g<S, MC, CG>(kr, cv);
+        const S den = rdot_g<S, MC, CG>(kr, vpp);
+        const S gs = first ? rowB[il] : S(0);
+        const S h = ut[r] * (gs - ut[r] * sig);
+#pragma unroll
+        for (int j = 0; j < MC; ++j) {
+          A[r][j] = fma(-ut[r], cv[j], A[r][j]);
+          A[r][j] = fma(-h, vp[j], A[r][j]);
+          c[j] = fma(kr[j], h, c[j]);
+        }
+        ut[r] = (ok(r) && t >= 2) ? F::rcp_fast(den) : S(0);
+      }
+      if (t >= 2) {
+        reduce_cols(c, [&](int k, S tot) {
+          const S vpk = vh[size_t(t - 1) * P + k];
+          vec0[k] = mul_(mul_(vpk, -mul_(vpk, tot)), inv_mass(k));
+        });
+      }
+    }
+    // gK = W + K~ .* G over the tile
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int il = lrow(r);
+      S kr[MC], gk[MC];
+      ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+      const S uT = rowA[il];
+      const S rr = ok(r) ? relu[il] : S(0);
+      const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
+      const S inv_imp = S(1.0 / double(imp_i));
+#pragma unroll
+      for (int j = 0; j < MC; ++j) {
+        const S W = (col(j) < m - 1) ? mul_(gx_of(rr, ex[j], imp_i, inv_imp), mul_(mul_(kr[j], uT), vT[j])) : S(0);
+        gk[j] = fma(kr[j], A[r][j], W);
+      }
+      st_seg<S, MC>(Kt + size_t(il) * P + g * MC, gk);
+    }
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
+    __syncthreads();
+    // ---- Adam ascent on this CTA's cells ----
+    const int s = a.state[ST_STEP];
+    const S bc1 = S(a.bc[2 * s]), bc2 = S(a.bc[2 * s + 1]);
+    const S ibc1 = S(1.0 / a.bc[2 * s]), ibc2 = S(1.0 / a.bc[2 * s + 1]);
+    auto adam = [&](S& cc, S& mm, S& vv, S gk) {
+      const S gg = mul_(gk, a.nie);
+      mm = add_(mul_(a.b1, mm), mul_(a.omb1, gg));
+      vv = add_(mul_(a.b2, vv), mul_(mul_(a.omb2, gg), gg));
+      S mh, vhat;
+      if constexpr (sizeof(S) == 4) {
+        mh = mul_(mm, ibc1);
+        vhat = mul_(vv, ibc2);
+      } else {
+        mh = F::div(mm, bc1);
+        vhat = F::div(vv, bc2);
+      }
+      cc = add_(cc, fdiv_<S>(mul_(a.lr, mh), add_(fsqrt_<S>(vhat), a.aeps)));
+    };
+    foreach_cell([&](int e0, int q) {
+      int i = e0 / m, k = e0 - i * m;
+      if (q >= 0) {
+        V16<S> c, mm, vv;
+        c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
+        mm.v = reinterpret_cast<const V16<S>*>(mu)[q].v;
+        vv.v = reinterpret_cast<const V16<S>*>(vu)[q].v;
+#pragma unroll
+        for (int j = 0; j < V; ++j) {
+          S& slot = Kt[i * P + k];
+          adam(c.s[j], mm.s[j], vv.s[j], slot);
+          slot = mul_(c.s[j], a.nie);
+          if (++k == m) { k = 0; ++i; }
+        }
+        reinterpret_cast<V16<S>*>(Cu)[q].v = c.v;
+        reinterpret_cast<V16<S>*>(mu)[q].v = mm.v;
+        reinterpret_cast<V16<S>*>(vu)[q].v = vv.v;
+      } else {
+        S c = Cu[e0], mm = mu[e0], vv = vu[e0];
+        S& slot = Kt[i * P + k];
+        adam(c, mm, vv, slot);
+        slot = mul_(c, a.nie);
+        Cu[e0] = c;
+        mu[e0] = mm;
+        vu[e0] = vv;
+      }
+    });
+  } else {
+    // INIT (C0 = -eps log uniform, lvi = 0) or RESUME (given C, lvi in beta)
+    const bool init = phase == PHASE_INIT;
+    if (!init && tid < m) vec2[tid] = a.beta[size_t(u) * m + tid];
+    for (int e = tid; e < ncell; e += NT) {
+      const int i = e / m, k = e - i * m;
+      S c0;
+      if (init) {
+        c0 = (k == m - 1) ? a.c_dummy : a.c_real;
+        Cu[e] = c0;
+        mu[e] = S(0);
+        vu[e] = S(0);
+      } else {
+        c0 = Cu[e];
+      }
+      Kt[i * P + k] = mul_(c0, a.nie);
+    }
+  }
+  __syncthreads();
+
+  // ---- forward: absorb beta = lvi, alpha = -rowmax(K + beta); T iterations ----
+  if (rank == 0 && tid < m) {
+    a.beta[size_t(u) * m + tid] = vec2[tid];
+    hu[tid] = S(1);
+  }
+  if (tid < m) vec0[tid] = S(1);
+  {
+    S bt[MC];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) bt[j] = vec2[col(j)];
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      const int il = lrow(r);
+      S kr[MC];
+      ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+      S mx = F::ninf();
+#pragma unroll
+      for (int j = 0; j < MC; ++j)
+        if (col(j) < m) mx = fmax(mx, add_(kr[j], bt[j]));
+      mx = group_max<S, CG>(mx);
+      const S al = -mx;
+      if (g == 0 && ok(r)) a.alpha[size_t(u) * n + r0 + il] = al;
+#pragma unroll
+      for (int j = 0; j < MC; ++j) kr[j] = (ok(r) && col(j) < m) ? F::exp_fast(add_(add_(kr[j], bt[j]), al)) : S(0);
+      st_seg<S, MC>(Kt + size_t(il) * P + g * MC, kr);
+    }
+  }
+  __syncthreads();
+  S A[R][MC];
+  S ut[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    ld_seg<S, MC>(A[r], Kt + size_t(lrow(r)) * P + g * MC);
+    ut[r] = S(0);
+  }
+  for (int t = 1; t <= T; ++t) {
+    S vv[MC], c[MC];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const S rp = F::rcp_fast(rdot_g<S, MC, CG>(A[r], vv));
+      ut[r] = ok(r) ? rp : S(0);
+    }
+#pragma unroll
+    for (int j = 0; j < MC; ++j) {
+      c[j] = A[0][j] * ut[0];
+#pragma unroll
+      for (int r = 1; r < R; ++r) c[j] = fma(A[r][j], ut[r], c[j]);
+    }
+    reduce_cols(c, [&](int k, S tot) {
+      const S vn = F::div_fast(mass(k), tot);
+      vec0[k] = vn;
+      if (rank == 0) hu[size_t(t) * m + k] = vn;
+    });
+  }
+  // per-item impact terms, float64, completed across the group
+  {
+    S vv[MC];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int il = lrow(r);
+      const double rr = ok(r) ? double(relu[il]) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int j = 0; j < MC; ++j)
+        if (col(j) < m - 1) acc = fma(rr * a.expo_d[min(col(j), m - 2)], double(mul_(mul_(A[r][j], ut[r]), vv[j])), acc);
+      acc = group_sum<double, CG>(acc);
+      if (g == 0 && ok(r)) a.partial[size_t(u) * n + r0 + il] = acc;
+    }
+  }
+  cluster.sync();   // keep every CTA's shared memory alive until remote reads are done
+}
+
+}  // namespace nsw

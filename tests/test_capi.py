@@ -46,7 +46,7 @@ def test_supported_variants(dtype, n, m, T):
 
 def test_unsupported_shapes_reported():
     lib = _lib.load()
-    assert lib.nsw_supported(0, 100, 40, 10) == 0    # m > 32: no tile yet
+    assert lib.nsw_supported(0, 100, 60, 10) == 0    # m > 52: no tile yet
 
 
 def _create(rel, expo, n, m, cfg, opt):
