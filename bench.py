@@ -241,7 +241,11 @@ def run_ours(a):
     from paper_2406_10262_b200.solver import DeviceSolver, solve_fair_ranking
 
     cfg = BASELINE_CONFIGS[a.config]
-    rel, expo, _ = make_instance(a.config, seed=0, num_users=a.users)
+    if a.slice:
+        lo, hi = (int(x) for x in a.slice.split(":"))
+        rel, expo, _ = make_instance(a.config, seed=0, user_slice=(lo, hi))
+    else:
+        rel, expo, _ = make_instance(a.config, seed=0, num_users=a.users)
     U, n, m, T = rel.shape[0], cfg.num_items, cfg.num_positions, a.inner or cfg.inner_iters
     opts = DeviceOptions(dtype=a.dtype, schedule="fixed", device=local, variant=a.variant)
     scfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=a.warmup + a.steps + 2,
@@ -373,6 +377,7 @@ def main(argv=None):
     ap.add_argument("--users", type=int, default=None)
     ap.add_argument("--inner", type=int, default=None)
     ap.add_argument("--variant", type=int, default=-1)
+    ap.add_argument("--slice", default=None, help="START:STOP users of the full instance (e.g. one GPU's shard)")
     a = ap.parse_args(argv)
     if a.dtype is None:
         a.dtype = BASELINE_CONFIGS[a.config].dtype
