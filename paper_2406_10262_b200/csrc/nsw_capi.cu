@@ -100,6 +100,7 @@ struct nsw_solver {
   const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
   size_t smem2 = 0;
   int U1 = 0;                     // users in the main launch (U1 == U: no tail launch)
+  int imp_chunks = 1;             // user chunks of the impact reduction
   // device state
   void *C = nullptr, *am = nullptr, *av = nullptr, *alpha = nullptr, *beta = nullptr, *hist = nullptr,
        *xbest = nullptr, *rel = nullptr, *expo = nullptr;
@@ -241,14 +242,19 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   return NSW_OK;
 }
 
-nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
-  nsw_status e = launch_fused(s, st);
-  if (e != NSW_OK) return e;
-  impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n,
-                                                                                  s->imp_local, s->state, s->tol);
+nsw_status launch_impact_reduce(nsw_solver* s, cudaStream_t st) {
+  const dim3 grid((s->n + IMP_ITEMS - 1) / IMP_ITEMS, s->imp_chunks);
+  impact_reduce_kernel<<<grid, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n, s->imp_chunks, s->split, s->counter,
+                                                     s->imp_local, s->state, s->tol);
   CUDA_TRY(cudaGetLastError());
   s->launches += 1;
   return NSW_OK;
+}
+
+nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
+  nsw_status e = launch_fused(s, st);
+  if (e != NSW_OK) return e;
+  return launch_impact_reduce(s, st);
 }
 
 nsw_status launch_finalize(nsw_solver* s, cudaStream_t st) {
@@ -368,6 +374,9 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->expo, size_t(m) * es);
   ALLOC(s->expo_d, size_t(m) * 8);
   ALLOC(s->partial, size_t(users_local) * n * 8);
+  // impact reduction: ~2 CTAs per SM of (8 items x user chunk)
+  s->imp_chunks = std::max(1, std::min(std::min(users_local, 64), (2 * 148 * IMP_ITEMS + n - 1) / n));
+  ALLOC(s->split, size_t(s->imp_chunks) * n * 8);
   ALLOC(s->own_imp_local, size_t(n) * 8);
   ALLOC(s->own_imp_all, size_t(world) * n * 8);
   ALLOC(s->imp_cur, size_t(n) * 8);
@@ -763,8 +772,8 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
     nsw_status e = launch_fused(s, s->stream);
     if (e != NSW_OK) return e;
     CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
-    impact_reduce_kernel<<<(s->n + IMP_ITEMS - 1) / IMP_ITEMS, IMP_THREADS, 0, s->stream>>>(
-        s->partial, s->U, s->n, s->imp_local, s->state, s->tol);
+    e = launch_impact_reduce(s, s->stream);
+    if (e != NSW_OK) return e;
     finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));

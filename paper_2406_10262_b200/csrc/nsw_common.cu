@@ -14,28 +14,34 @@ __device__ __forceinline__ bool forward_ready(int phase, int tol_mode) {
                   : (phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME);
 }
 
-// One CTA per IMP_ITEMS consecutive items; its 256 threads stride over the
-// users (thread t: item t % IMP_ITEMS, user lane t / IMP_ITEMS), then a fixed
-// shared-memory tree combines the lanes: one pass, deterministic order.
+// Two-level, fixed-order reduction.  Level 1: CTA (x, y) sums items
+// [8x, 8x+8) over user chunk y (thread t: item t % IMP_ITEMS, user lane
+// t / IMP_ITEMS, then a fixed shared-memory tree) into split[y][i].  Level
+// 2: the last CTA to finish sums the chunks in chunk order.
 __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double* __restrict__ partial, int U,
-                                                                    int n, double* __restrict__ imp_local,
+                                                                    int n, int chunks, double* __restrict__ split,
+                                                                    unsigned int* counter,
+                                                                    double* __restrict__ imp_local,
                                                                     const int* __restrict__ state, int tol_mode) {
   if (!forward_ready(state[ST_PHASE], tol_mode)) return;
   constexpr int LANES = IMP_THREADS / IMP_ITEMS;
   __shared__ double red[IMP_THREADS];
+  __shared__ bool last;
   const int j = threadIdx.x % IMP_ITEMS;
   const int l = threadIdx.x / IMP_ITEMS;
   const int i = blockIdx.x * IMP_ITEMS + j;
+  const int y = blockIdx.y;
+  const int ub = int((long long)y * U / chunks), ue = int((long long)(y + 1) * U / chunks);
   double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
   if (i < n) {
-    int u = l;
-    for (; u + 3 * LANES < U; u += 4 * LANES) {
+    int u = ub + l;
+    for (; u + 3 * LANES < ue; u += 4 * LANES) {
       a0 += partial[size_t(u) * n + i];
       a1 += partial[size_t(u + LANES) * n + i];
       a2 += partial[size_t(u + 2 * LANES) * n + i];
       a3 += partial[size_t(u + 3 * LANES) * n + i];
     }
-    for (; u < U; u += LANES) a0 += partial[size_t(u) * n + i];
+    for (; u < ue; u += LANES) a0 += partial[size_t(u) * n + i];
   }
   red[threadIdx.x] = (a0 + a1) + (a2 + a3);
   __syncthreads();
@@ -43,7 +49,19 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
     if (l < w) red[threadIdx.x] += red[threadIdx.x + w * IMP_ITEMS];
     __syncthreads();
   }
-  if (l == 0 && i < n) imp_local[i] = red[threadIdx.x];
+  if (l == 0 && i < n) split[size_t(y) * n + i] = red[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x * gridDim.y - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int ii = threadIdx.x; ii < n; ii += IMP_THREADS) {
+    double acc = 0.0;
+    for (int c = 0; c < chunks; ++c) acc += __ldcg(split + size_t(c) * n + ii);
+    imp_local[ii] = acc;
+  }
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 __global__ void __launch_bounds__(256) tol_check_kernel(const double* __restrict__ res, int U, int T, int chunk,

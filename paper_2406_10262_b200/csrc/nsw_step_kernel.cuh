@@ -673,7 +673,8 @@ forward_iterations:
 // --------------------------------------------------------------------------
 constexpr int IMP_THREADS = 256;
 constexpr int IMP_ITEMS = 8;
-__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n,
+__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n, int chunks,
+                                     double* __restrict__ split, unsigned int* counter,
                                      double* __restrict__ imp_local, const int* __restrict__ state, int tol_mode);
 
 // Tolerance mode: after each forward chunk, the lock-step stopping test of
