@@ -62,10 +62,12 @@ struct Fp<float> {
   }
   static __device__ __forceinline__ float log_(float x) { return logf(x); }
   static __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
-  // hot-loop reciprocal: one MUFU.RCP (<= 1 ulp), no IEEE fix-up branch
+  // hot-loop reciprocal: one MUFU.RCP (<= 1 ulp), no IEEE fix-up branch.
+  // volatile: executed unconditionally, so a select on its result is an
+  // FSEL rather than a branch around the asm block.
   static __device__ __forceinline__ float rcp_fast(float x) {
     float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    asm volatile("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
   }
   static __device__ __forceinline__ float div(float a, float b) { return __fdiv_rn(a, b); }

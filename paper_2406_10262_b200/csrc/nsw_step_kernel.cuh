@@ -167,6 +167,13 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* hu = a.hist + size_t(u) * (T + 1) * m;
   const S* relu = a.rel + size_t(u) * n;
   auto ok = [&](int r) { return tid + r * NT < n; };
+  // 1/x on live rows, 0 on padding rows, as arithmetic (no branch): a select
+  // lets the compiler branch around the whole row dot, which splits the row
+  // loop into basic blocks and serialises the rows' FMA chains.
+  auto masked_rcp = [&](S x, bool live) -> S {
+    const S on = live ? S(1) : S(0);
+    return F::rcp_fast(x + (S(1) - on)) * on;
+  };
   // K~ = exp(K + beta_k + alpha_i), K = C * (-1/eps) (solver.py:188); the one
   // expression used by both the forward and the backward's rebuild, so K~ is
   // bit-identical in both.
@@ -391,7 +398,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           A[r][k] = fma(-h, vp[k], A[r][k]);
           c[k] = fma(kr[k], h, c[k]);
         }
-        ut[r] = (ok(r) && replay) ? F::rcp_fast(den) : S(0);
+        ut[r] = masked_rcp(den, ok(r) && replay);
       }
       if (t >= 2) {
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
@@ -590,7 +597,7 @@ forward_iterations:
         for (int r = 0; r < R; ++r) {
           const S sr = rdot<S, M>(A[r], vv);
           if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
-          ut[r] = ok(r) ? F::rcp_fast(sr) : S(0);
+          ut[r] = masked_rcp(sr, ok(r));
         }
         if constexpr (TOLM) {
           rmax = warp_max(rmax);
