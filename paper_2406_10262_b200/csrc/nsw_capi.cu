@@ -53,6 +53,15 @@ int sizeof_dtype(int dt) { return dt == NSW_F64 ? 8 : 4; }
 const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
   auto& reg = variant_registry();
   std::vector<const Variant*> c;
+  if (forced == -2 && dtype == NSW_F32) {
+    // tensor-core adjoint tiles (registered under dtype 2), smallest fitting
+    const Variant* best = nullptr;
+    for (auto& v : reg)
+      if (v.dtype == 2 && v.M >= m && v.rows >= n && v.smem(T) <= kMaxSmem)
+        if (!best || v.M < best->M || (v.M == best->M && v.rows < best->rows)) best = &v;
+    if (best) return best;
+    forced = -1;
+  }
   // one-CTA-per-user tiles first; cluster tiles (CL > 1 CTAs per user) only
   // when no single-CTA tile holds the user's n x m tile
   for (int pass = 0; pass < 2 && c.empty(); ++pass)
@@ -83,7 +92,8 @@ const Variant* choose_wide_variant(const Variant* base, int n, int T) {
   const Variant* best = nullptr;
   auto score = [](const Variant* v) { return std::abs(v->R - 2) * 4096 + v->NT; };
   for (auto& v : variant_registry())
-    if (v.dtype == base->dtype && v.M == base->M && v.CL == 1 && v.rows >= n && v.smem(T) <= kMaxSmem)
+    if (v.dtype == (base->dtype == 2 ? 0 : base->dtype) && v.M == base->M && v.CL == 1 && v.rows >= n &&
+        v.smem(T) <= kMaxSmem)
       if (!best || score(&v) < score(best)) best = &v;
   return best;
 }
@@ -413,7 +423,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is not available for cluster tiles (m > 32 or large n)");
   }
-  if (options->variant < 0 && var->CL == 1) {
+  if (options->variant == -1 && var->CL == 1) {
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);

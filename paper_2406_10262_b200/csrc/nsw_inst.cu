@@ -8,6 +8,13 @@
 #ifndef NSW_M
 #error "NSW_M must be defined"
 #endif
+// tensor-core adjoint variants (tcgen05 + TMEM), fp32 only; registered with
+// dtype 2 so the default chooser skips them until selected explicitly
+#define NSW_REG_TC(R, NT, MINB)                                                                        \
+  Registrar NSW_CAT(regtc_, __LINE__)(Variant{2, NSW_M, R, NT,                                         \
+                                              (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB, true>, \
+                                              &smem_tc_of<R, NT>});
+
 #if NSW_F64
 #define NSW_S double
 #define NSW_DT 1
@@ -22,6 +29,10 @@ namespace {
 template <int R, int NT>
 size_t smem_of(int T) {
   return step_smem_bytes<NSW_S, NSW_M, R, NT>(T);
+}
+template <int R, int NT>
+size_t smem_tc_of(int T) {
+  return step_smem_bytes<NSW_S, NSW_M, R, NT, true>(T);
 }
 
 #define NSW_CAT2(a, b) a##b
@@ -49,6 +60,7 @@ NSW_REG(2, 512, 1)
 #endif
 #else
 #if NSW_M <= 11
+NSW_REG_TC(4, 128, 4)
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)

@@ -86,12 +86,68 @@ struct RowSlots {
   static constexpr bool kPad = P > M;
 };
 
-template <typename S, int M, int R, int NT>
+template <typename S, int M, int R, int NT, bool TC = false>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
-                      size_t(NT / 32) + 2);
+                      size_t(NT / 32) + 4) +
+         (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 / TMEM helpers (sm_100a) for the tensor-core adjoint accumulation
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+// K-major, no-swizzle UMMA shared-memory descriptor: core matrices of
+// 8 rows x 16 bytes; LBO = stride between the two 16-byte K chunks, SBO =
+// stride between 8-row groups (both >> 4), version 1 (Blackwell).
+__device__ __forceinline__ uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, M=128, N=16
+constexpr uint32_t kIdescTf32_128x16 = (1u << 4) | (2u << 7) | (2u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(accum), "r"(kIdescTf32_128x16), "r"(0u));
+}
+__device__ __forceinline__ void umma_commit(uint32_t mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+               "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7]),
+        "=f"(v[8]), "=f"(v[9]), "=f"(v[10]), "=f"(v[11]), "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(taddr)
+      : "memory");
 }
 
 // fp32 throughput path: divisions / square roots off the hot path use the
@@ -119,8 +175,11 @@ __device__ __forceinline__ S fsqrt_(S x) {
 // policy write) or as loops over this thread's rows (seed, log-domain
 // iteration 1); only the two hot loops (forward iterations 2..T and the T
 // reverse levels) hold the R x M tile in registers.
-template <typename S, int M, int R, int NT, int MINB>
+template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
+  // TC: the backward's adjoint G accumulates in tensor memory through tcgen05
+  // MMAs (fp32 path, 4-warp CTAs, M <= 16) instead of 2 FFMAs per cell-level.
+  static_assert(!TC || (sizeof(S) == 4 && NT == 128 && M <= 16 && R <= 4), "tensor-core tile shape");
   using F = Fp<S>;
   constexpr int P = Pitch<S, M>::value;
   constexpr bool PAD = RowSlots<S, M>::kPad;
@@ -139,6 +198,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* rowB = rowA + (PAD ? 0 : size_t(NT) * R);
   S* colres = rowB + (PAD ? 0 : size_t(NT) * R);  // [2][P] column residuals (tolerance mode)
   S* redmax = colres + 2 * P;                     // [NW] per-warp row-residual maxima
+  // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
+  unsigned char* tc_base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(redmax + NW + 4) + 127) & ~uintptr_t(127));
+  float* Bop = reinterpret_cast<float*>(tc_base);            // [2][2][16 x 8]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tc_base + 2048);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_base + 2056);
   // slotA: alpha -> u~^T -> u^1 ; slotB: seed g_u (shares slotA's storage
   // when PAD: written after u~^T is in registers, u~^T restored at level T)
   auto slotA = [&](int i) -> S& { return PAD ? Kt[size_t(i) * P + M] : rowA[i]; };
@@ -326,105 +391,289 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     __syncthreads();
 
     // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
-    S A[R][M];  // adjoint G: gK = W + K~ .* G
-    S ut[R];
-    {
-      S c[M];
+    if constexpr (TC) {
+      // ---------------- tensor-core adjoint --------------------------------
+      // G (512 x 16, fp32) lives in TMEM as 4 blocks of 128 lanes x 16
+      // columns (row tid + r*128 = block r, lane tid).  Every 4 levels the
+      // rank-8 update G -= [u~ h]_levels [cv v~^{t-1}]'_levels is one
+      // 128x16x8 tf32 MMA per block, split 3xTF32 (hi*hi + hi*lo + lo*hi)
+      // for fp32 accuracy.  A (u~, h pairs) goes registers -> TMEM
+      // (tcgen05.st), B (the column vectors) shared memory; K~ stays in
+      // registers for the whole sweep.
+      const int warp_id = tid >> 5;
+      const uint32_t lane_base = uint32_t(32 * (warp_id & 3)) << 16;
+      if (warp_id == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+      }
+      if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
+      for (int q = tid; q < 2 * 2 * 128; q += NT) Bop[q] = 0.f;
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t tmem = *tmem_slot;   // column base; D blocks at +16b, A_hi +64+8b, A_lo +96+8b
+      const uint32_t mb = smem_u32(mbar);
+
+      S Kr[R][M];
+      S ut[R];
+      float av[R][8];
+      {
+        S c[M];
 #pragma unroll
-      for (int k = 0; k < M; ++k) c[k] = S(0);
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          lds_vec<S, M>(Kr[r], Kt + size_t(i) * P);
+          ut[r] = slotA(i);
+          const S rr = ok(r) ? relu[i] : S(0);
+          const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+          const S inv_imp = S(1.0 / double(imp_i));
+          S gsum = S(0);
+#pragma unroll
+          for (int k = 0; k < M; ++k) {
+            if (k < m - 1) {
+              const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), mul_(mul_(Kr[r][k], ut[r]), vT[k]));
+              gsum += W;
+              c[k] += W;
+            }
+          }
+          slotB(i) = gsum;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) av[r][q] = 0.f;
+        }
+        cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+          vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));
+        });
+      }
+      int chunk = 0, buf = 0;
+      for (int t = Th; t >= 1; --t) {
+        const int j = (Th - t) & 3;       // slot of this level in the current chunk
+        S cv[M], vpp[M], c[M];
+        lds_vec<S, M>(cv, vec0);
+        lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
+        if (tid < 16) {                   // B rows: -cv^t and -v~^{t-1} of column tid
+          const float x0 = tid < m ? -vec0[tid] : 0.f;
+          const float x1 = tid < m ? -vh[size_t(t - 1) * P + tid] : 0.f;
+          float* bh = Bop + (buf * 2 + 0) * 128;
+          float* bl = Bop + (buf * 2 + 1) * 128;
+          const int o0 = (tid & 7) * 4 + (tid >> 3) * 64 + (j >> 1) * 32 + (j & 1) * 2;
+          const float h0 = to_tf32(x0), h1 = to_tf32(x1);
+          bh[o0] = h0;
+          bh[o0 + 1] = h1;
+          bl[o0] = to_tf32(x0 - h0);
+          bl[o0 + 1] = to_tf32(x1 - h1);
+        }
+        const bool first = t == Th;
+        const bool replay = t >= 2;
+#pragma unroll
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          const S sig = rdot<S, M>(Kr[r], cv);
+          const S den = rdot<S, M>(Kr[r], vpp);
+          S gs = S(0);
+          if (first) {
+            gs = slotB(i);
+            slotA(i) = ut[r];
+          }
+          const S h = ut[r] * (gs - ut[r] * sig);
+#pragma unroll
+          for (int k = 0; k < M; ++k) c[k] = fma(Kr[r][k], h, c[k]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (q == j) {
+              av[r][2 * q] = ut[r];
+              av[r][2 * q + 1] = h;
+            }
+          }
+          ut[r] = masked_rcp(den, ok(r) && replay);
+        }
+        if (t >= 2) {
+          cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+            const S vpk = vh[size_t(t - 1) * P + k];
+            const S gv = -mul_(vpk, tot);
+            vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+          });
+        }
+        if (j == 3 || t == 1) {
+          // flush the chunk: A -> TMEM, then one elected thread issues the MMAs
+          if (chunk > 0) mbar_wait(mb, uint32_t((chunk - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            float hi[8], lo[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              hi[q] = to_tf32(av[r][q]);
+              lo[q] = to_tf32(av[r][q] - hi[q]);
+              av[r][q] = 0.f;
+            }
+            tmem_st8(tmem + lane_base + uint32_t(64 + 8 * r), hi);
+            tmem_st8(tmem + lane_base + uint32_t(96 + 8 * r), lo);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncthreads();
+          if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint64_t bh = umma_desc_kmajor(smem_u32(Bop + (buf * 2 + 0) * 128), 128, 256);
+            const uint64_t bl = umma_desc_kmajor(smem_u32(Bop + (buf * 2 + 1) * 128), 128, 256);
+#pragma unroll
+            for (int b = 0; b < R; ++b) {
+              const uint32_t d = tmem + uint32_t(16 * b);
+              const uint32_t ah = tmem + uint32_t(64 + 8 * b), al = tmem + uint32_t(96 + 8 * b);
+              umma_tf32_ts(d, ah, bh, chunk > 0 ? 1u : 0u);
+              umma_tf32_ts(d, ah, bl, 1u);
+              umma_tf32_ts(d, al, bh, 1u);
+            }
+            umma_commit(mb);
+          }
+          ++chunk;
+          buf ^= 1;
+          if (tid < 16) {   // the next chunk's B buffer starts from zero (short final chunk)
+            float* bh = Bop + (buf * 2 + 0) * 128;
+            float* bl = Bop + (buf * 2 + 1) * 128;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int o = (tid & 7) * 4 + (tid >> 3) * 64 + (q >> 1) * 32 + (q & 1) * 2;
+              bh[o] = bh[o + 1] = 0.f;
+              bl[o] = bl[o + 1] = 0.f;
+            }
+          }
+        }
+      }
+      mbar_wait(mb, uint32_t((chunk - 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      // gK = W + K~ .* G, G read back from TMEM
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
-        S kr[M];
-        lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        ut[r] = slotA(i);
+        float g16[16];
+        tmem_ld16(tmem + lane_base + uint32_t(16 * r), g16);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        S gk[M];
+        const S uT = slotA(i);
         const S rr = ok(r) ? relu[i] : S(0);
         const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
         const S inv_imp = S(1.0 / double(imp_i));
-        S gsum = S(0);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          A[r][k] = S(0);
-          if (k < m - 1) {
-            const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
-            const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), X);
-            gsum += W;
-            c[k] += W;
+          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), mul_(mul_(Kr[r][k], uT), vT[k])) : S(0);
+          gk[k] = fma(Kr[r][k], S(g16[k]), W);
+        }
+        sts_vec<S, M>(Kt + size_t(i) * P, gk);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncthreads();
+      if (warp_id == 0) {
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+      }
+    } else {
+    S A[R][M];  // adjoint G: gK = W + K~ .* G
+      S ut[R];
+      {
+        S c[M];
+  #pragma unroll
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+  #pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          S kr[M];
+          lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          ut[r] = slotA(i);
+          const S rr = ok(r) ? relu[i] : S(0);
+          const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+          const S inv_imp = S(1.0 / double(imp_i));
+          S gsum = S(0);
+  #pragma unroll
+          for (int k = 0; k < M; ++k) {
+            A[r][k] = S(0);
+            if (k < m - 1) {
+              const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
+              const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), X);
+              gsum += W;
+              c[k] += W;
+            }
           }
+          slotB(i) = gsum;
         }
-        slotB(i) = gsum;
-      }
-      cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-        vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
-      });
-    }
-
-    // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
-    //   g_u  <- [t==T] g_u^seed - u~ (K~ cv)_i                  column VJP
-    //   h    <- u~ g_u
-    //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
-    //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
-    //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 2)
-    for (int t = Th; t >= 1; --t) {
-      S cv[M], vp[M], c[M];
-      lds_vec<S, M>(cv, vec0);
-      lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
-      const S* vppp = vh + size_t(t >= 2 ? t - 2 : 0) * P;
-      const bool first = t == Th;
-      const bool replay = t >= 2;
-#pragma unroll
-      for (int k = 0; k < M; ++k) c[k] = S(0);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = tid + r * NT;
-        S kr[M];
-        lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        const S sig = rdot<S, M>(kr, cv);
-        S den;
-        {
-          S vpp[M];
-          lds_vec<S, M>(vpp, vppp);
-          den = rdot<S, M>(kr, vpp);
-        }
-        S gs = S(0);
-        if (first) {
-          gs = slotB(i);
-          slotA(i) = ut[r];   // restore u~^T for the gK epilogue
-        }
-        const S h = ut[r] * (gs - ut[r] * sig);
-#pragma unroll
-        for (int k = 0; k < M; ++k) {
-          A[r][k] = fma(-ut[r], cv[k], A[r][k]);
-          A[r][k] = fma(-h, vp[k], A[r][k]);
-          c[k] = fma(kr[k], h, c[k]);
-        }
-        ut[r] = masked_rcp(den, ok(r) && replay);
-      }
-      if (t >= 2) {
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-          const S vpk = vh[size_t(t - 1) * P + k];
-          const S gv = -mul_(vpk, tot);
-          vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+          vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
         });
       }
-    }
-    // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = tid + r * NT;
-      S kr[M], gk[M];
-      lds_vec<S, M>(kr, Kt + size_t(i) * P);
-      const S uT = slotA(i);
-      const S rr = ok(r) ? relu[i] : S(0);
-      const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
-      const S inv_imp = S(1.0 / double(imp_i));
-#pragma unroll
-      for (int k = 0; k < M; ++k) {
-        const S X = mul_(mul_(kr[k], uT), vT[k]);
-        const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), X) : S(0);
-        gk[k] = fma(kr[k], A[r][k], W);
+  
+      // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
+      //   g_u  <- [t==T] g_u^seed - u~ (K~ cv)_i                  column VJP
+      //   h    <- u~ g_u
+      //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
+      //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
+      //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 2)
+      for (int t = Th; t >= 1; --t) {
+        S cv[M], vp[M], c[M];
+        lds_vec<S, M>(cv, vec0);
+        lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
+        const S* vppp = vh + size_t(t >= 2 ? t - 2 : 0) * P;
+        const bool first = t == Th;
+        const bool replay = t >= 2;
+  #pragma unroll
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+  #pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          S kr[M];
+          lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          const S sig = rdot<S, M>(kr, cv);
+          S den;
+          {
+            S vpp[M];
+            lds_vec<S, M>(vpp, vppp);
+            den = rdot<S, M>(kr, vpp);
+          }
+          S gs = S(0);
+          if (first) {
+            gs = slotB(i);
+            slotA(i) = ut[r];   // restore u~^T for the gK epilogue
+          }
+          const S h = ut[r] * (gs - ut[r] * sig);
+  #pragma unroll
+          for (int k = 0; k < M; ++k) {
+            A[r][k] = fma(-ut[r], cv[k], A[r][k]);
+            A[r][k] = fma(-h, vp[k], A[r][k]);
+            c[k] = fma(kr[k], h, c[k]);
+          }
+          ut[r] = masked_rcp(den, ok(r) && replay);
+        }
+        if (t >= 2) {
+          cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+            const S vpk = vh[size_t(t - 1) * P + k];
+            const S gv = -mul_(vpk, tot);
+            vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+          });
+        }
       }
-      sts_vec<S, M>(Kt + size_t(i) * P, gk);
+      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
+  #pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        S kr[M], gk[M];
+        lds_vec<S, M>(kr, Kt + size_t(i) * P);
+        const S uT = slotA(i);
+        const S rr = ok(r) ? relu[i] : S(0);
+        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
+        const S inv_imp = S(1.0 / double(imp_i));
+  #pragma unroll
+        for (int k = 0; k < M; ++k) {
+          const S X = mul_(mul_(kr[k], uT), vT[k]);
+          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), X) : S(0);
+          gk[k] = fma(kr[k], A[r][k], W);
+        }
+        sts_vec<S, M>(Kt + size_t(i) * P, gk);
+      }
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
     __syncthreads();

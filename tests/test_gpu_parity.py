@@ -88,15 +88,18 @@ def _resume_step(rel, expo, p, state, step, opts):
     return out
 
 
-@pytest.mark.parametrize("dtype,tol_x,tol_c", [("float64", 1e-12, 1e-11), ("float32", 2e-6, 5e-6)])
-def test_one_step_from_oracle_state(golden, dtype, tol_x, tol_c):
+@pytest.mark.parametrize("dtype,tol_x,tol_c,variant", [("float64", 1e-12, 1e-11, -1), ("float32", 2e-6, 5e-6, -1),
+                                                       ("float32", 2e-6, 5e-6, -2)])
+def test_one_step_from_oracle_state(golden, dtype, tol_x, tol_c, variant):
+    """variant -2 = the tensor-core adjoint tile (tcgen05.mma kind::tf32, 3xTF32
+    split, G accumulated in TMEM)."""
     g = golden("cfg0_fixed")
     rel, expo = g["relevance"], g["exposure"]
     p = orc.SolverParams(epsilon=0.1, sinkhorn_max_iters=50, outer_max_iters=12, grad_threshold=1e-300)
     _, _, states = orc.solve(rel, expo, p, record_states={10})
     st = states[10]
     ref = orc.one_step(rel, expo, st, p)
-    dev = _resume_step(rel, expo, p, st, 10, DeviceOptions(dtype=dtype, schedule="fixed"))
+    dev = _resume_step(rel, expo, p, st, 10, DeviceOptions(dtype=dtype, schedule="fixed", variant=variant))
     dx = np.abs(dev["plan"] - ref["plan"]).max()
     dc = np.abs(dev["cost"] - ref["cost"]).max()
     df = abs(dev["objective"] / st["objective"] - 1)
