@@ -150,6 +150,10 @@ int32_t nsw_solver_tail_users(nsw_solver* s);
 /* Device time (ms) of the last N fused step kernels, CUDA events. */
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused_kernel);
+/* Diagnostics: global-timer stamps (ns) of the fused kernel's phase
+ * boundaries, [count users][16], of the last step the solver ran.  Only when
+ * the environment had NSW_PHASE_TIMING=1 at nsw_solver_create. */
+nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count);
 
 /* ------------------------------------------------------------------------ *
  * 3. Inner operator seam (device pointers, fixed schedule).                *

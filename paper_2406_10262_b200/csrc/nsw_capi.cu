@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -73,7 +74,8 @@ const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
     if (a->M != b->M) return a->M < b->M;
     if (a->CL != b->CL) return a->CL < b->CL;
     if (a->rows != b->rows) return a->rows < b->rows;
-    return a->R > b->R;
+    if (a->R != b->R) return a->R > b->R;
+    return a->minb < b->minb;
   });
   if (forced >= 0) {
     // forced index counts over the candidates with the chosen M
@@ -136,6 +138,7 @@ struct nsw_solver {
   FinalizeArgs fin{};
   float* flush_buf = nullptr;
   size_t flush_n = 0;
+  unsigned long long* phase_ns = nullptr;  // [U][16] phase stamps (NSW_PHASE_TIMING diagnostics)
 };
 
 namespace {
@@ -178,6 +181,8 @@ void fill_step_args(nsw_solver* s, StepArgs<S>& a) {
   a.c_dummy = S(-eps * std::log(double(n - m + 1) / n));
   a.mass_dummy = S(n - m + 1);
   a.log_mass_dummy = S(std::log(double(n - m + 1)));
+  a.inv_mass_dummy = S(1.0 / double(n - m + 1));
+  a.phase_ns = s->phase_ns;
 }
 
 template <typename S>
@@ -399,6 +404,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->counter, 16);
   ALLOC(s->state, ST_WORDS * sizeof(int));
   ALLOC(s->iters, size_t(s->outer_max) * sizeof(int));
+  if (const char* pt = std::getenv("NSW_PHASE_TIMING"); pt && *pt && *pt != '0') {
+    ALLOC(s->phase_ns, size_t(users_local) * 16 * 8);
+    CUDA_TRY(cudaMemset(s->phase_ns, 0, size_t(users_local) * 16 * 8));
+  }
   s->tol = options->schedule == NSW_SCHEDULE_TOLERANCE;
   if (s->tol) ALLOC(s->res, size_t(users_local) * (T + 1) * 8);
 #undef ALLOC
@@ -506,7 +515,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
-                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters};
+                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters, s->phase_ns};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (s->state_host) cudaFreeHost(s->state_host);
@@ -801,6 +810,15 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
   for (auto& e : ev) cudaEventDestroy(e);
   if (ms_total) *ms_total = tot;
   if (ms_fused) *ms_fused = fus;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count) {
+  if (!s || !out) return fail(NSW_ERR_ARG, "NULL argument");
+  if (!s->phase_ns) return fail(NSW_ERR_UNSUPPORTED, "phase timing is off (set NSW_PHASE_TIMING=1 before creating the solver)");
+  const size_t words = size_t(std::min(count, s->U)) * 16;
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  CUDA_TRY(cudaMemcpy(out, s->phase_ns, words * 8, cudaMemcpyDeviceToHost));
   return NSW_OK;
 }
 

@@ -74,6 +74,7 @@ struct Fp<float> {
   static __device__ __forceinline__ float div_fast(float a, float b) { return a * rcp_fast(b); }
   static __device__ __forceinline__ float sqrt_(float x) { return __fsqrt_rn(x); }
   static __device__ __forceinline__ float ninf() { return -CUDART_INF_F; }
+  static __device__ __forceinline__ float tiny() { return 1.17549435e-38f; }  // FLT_MIN
   static constexpr int kVec = 4;  // elements per 16-byte vector
 };
 
@@ -88,6 +89,7 @@ struct Fp<double> {
   static __device__ __forceinline__ double div_fast(double a, double b) { return __ddiv_rn(a, b); }
   static __device__ __forceinline__ double sqrt_(double x) { return __dsqrt_rn(x); }
   static __device__ __forceinline__ double ninf() { return -CUDART_INF; }
+  static __device__ __forceinline__ double tiny() { return 2.2250738585072014e-308; }  // DBL_MIN
   static constexpr int kVec = 2;
 };
 

@@ -13,7 +13,7 @@
 #define NSW_REG_TC(R, NT, MINB)                                                                        \
   Registrar NSW_CAT(regtc_, __LINE__)(Variant{2, NSW_M, R, NT,                                         \
                                               (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB, true>, \
-                                              &smem_tc_of<R, NT>});
+                                              &smem_tc_of<R, NT>, 1, 0, MINB});
 
 #if NSW_F64
 #define NSW_S double
@@ -40,7 +40,7 @@ size_t smem_tc_of(int T) {
 #define NSW_REG(R, NT, MINB)                                                                        \
   Registrar NSW_CAT(reg_, __LINE__)(Variant{NSW_DT, NSW_M, R, NT,                                   \
                                             (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB>, \
-                                            &smem_of<R, NT>});
+                                            &smem_of<R, NT>, 1, 0, MINB});
 
 #if NSW_F64
 // parity instantiation: shapes up to 2048 (M <= 16) / 1024 (M <= 32) items
@@ -65,6 +65,7 @@ NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)
 NSW_REG(8, 64, 6)
+NSW_REG(8, 64, 7)
 NSW_REG(4, 128, 3)
 NSW_REG(8, 128, 3)
 NSW_REG(8, 256, 1)

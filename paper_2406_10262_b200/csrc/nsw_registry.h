@@ -15,6 +15,7 @@ struct Variant {
   size_t (*smem)(int T);
   int CL = 1;     // CTAs per user (thread-block cluster) ; 1 = one CTA per user
   int rows = 0;   // items per CTA (R * NT for the 1-D tiles)
+  int minb = 1;   // __launch_bounds__ min CTAs per SM (register cap)
 };
 
 std::vector<Variant>& variant_registry();

@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   auto ok = [&](int r) { return lrow(r) < nloc; };
   auto col = [&](int j) { return g * MC + j; };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
-  auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
+  auto inv_mass = [&](int k) -> S { return k == m - 1 ? a.inv_mass_dummy : S(1); };
   auto ktilde = [&](S c, S beta_k, S alpha_i) -> S {
     return F::exp_fast(add_(add_(mul_(c, a.nie), beta_k), alpha_i));
   };

@@ -41,6 +41,8 @@ struct StepArgs {
   S lr, b1, b2, omb1, omb2, aeps;
   S c_real, c_dummy;     // initial costs -eps*log(1/n), -eps*log((n-m+1)/n)
   S mass_dummy, log_mass_dummy;
+  S inv_mass_dummy;              // 1/(n-m+1), correctly rounded on the host
+  unsigned long long* phase_ns;  // [U][16] diagnostics: phase-boundary timestamps (nullptr: off)
 };
 
 template <typename S>
@@ -221,6 +223,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 
   const int u = a.user0 + blockIdx.x;
   const int tid = threadIdx.x;
+  // diagnostics: global-timer stamp of phase boundary p (thread 0; off unless
+  // the solver was created with NSW_PHASE_TIMING set)
+  auto mark = [&](int p) {
+    if (a.phase_ns != nullptr && tid == 0) a.phase_ns[size_t(u) * 16 + p] = globaltimer_ns();
+  };
+  mark(0);
   const int n = a.n, m = a.m;
   const int nm = n * m;
   const bool vec_ok = (nm % V) == 0;   // user tiles are 16-byte aligned
@@ -239,6 +247,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     const S on = live ? S(1) : S(0);
     return F::rcp_fast(x + (S(1) - on)) * on;
   };
+  // 1/x clamped away from 0: padding rows (all-zero K~ rows, x = 0) get a
+  // large finite value instead of inf, so u~ * 0 stays 0 without a mask.
+  auto rcp_clamped = [&](S x) -> S { return F::rcp_fast(fmax(x, F::tiny())); };
   // K~ = exp(K + beta_k + alpha_i), K = C * (-1/eps) (solver.py:188); the one
   // expression used by both the forward and the backward's rebuild, so K~ is
   // bit-identical in both.
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     return F::exp_fast(add_(add_(mul_(c, a.nie), beta_k), alpha_i));
   };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
-  auto inv_mass = [&](int k) -> S { return k == m - 1 ? F::rcp(a.mass_dummy) : S(1); };
+  auto inv_mass = [&](int k) -> S { return k == m - 1 ? a.inv_mass_dummy : S(1); };
   // gx = r e / Imp (solver.py:86-89); fp32 uses a per-row reciprocal
   auto gx_of = [&](S rr, S e, S imp_i, S inv_imp) -> S {
     if constexpr (sizeof(S) == 4) return mul_(mul_(rr, e), inv_imp);
@@ -277,9 +288,11 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     vec1[tid] = S(0);
     vec2[tid] = S(0);
   }
-  S ex[M];
+  // exposures, loaded where used so they are not live across the loops
+  auto load_ex = [&](S (&e)[M]) {
 #pragma unroll
-  for (int k = 0; k < M; ++k) ex[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
+    for (int k = 0; k < M; ++k) e[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
+  };
   __syncthreads();
 
   if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING || phase == PHASE_FWD_CONT || phase == PHASE_FWD_FIN) {
@@ -300,6 +313,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         if (idx0 + j * NT < (Th + 1) * P) vh[idx0 + j * NT] = hv[j];
     }
     __syncthreads();
+    mark(1);
     if (vec_ok) {
       const int nq = nm / V;
       for (int q0 = tid; q0 < nq; q0 += 8 * NT) {
@@ -326,6 +340,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       }
     }
     __syncthreads();
+    mark(2);
     S vT[M];
     lds_vec<S, M>(vT, vh + size_t(Th) * P);
     {
@@ -387,8 +402,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       goto forward_iterations;
     }
     __syncthreads();
+    mark(3);
     if (improved) write_policy();   // best-so-far policy is step k-1's (solver.py:217-219)
     __syncthreads();
+    mark(4);
 
     // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
     if constexpr (TC) {
@@ -419,7 +436,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       S ut[R];
       float av[R][8];
       {
-        S c[M];
+        S c[M], ex[M];
+        load_ex(ex);
 #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
@@ -549,6 +567,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       mbar_wait(mb, uint32_t((chunk - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
       // gK = W + K~ .* G, G read back from TMEM
+      S ex[M];
+      load_ex(ex);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
@@ -576,8 +596,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     } else {
     S A[R][M];  // adjoint G: gK = W + K~ .* G
       S ut[R];
+      S gs[R];    // seed g_u (row sums of W), live only until the first level
       {
-        S c[M];
+        S c[M], ex[M];
+        load_ex(ex);
   #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
   #pragma unroll
@@ -600,26 +622,32 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
               c[k] += W;
             }
           }
-          slotB(i) = gsum;
+          gs[r] = gsum;
         }
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
           vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
         });
       }
-  
+      mark(5);
+
       // Per level t, per row i (u~ = u~^t_i, cv = v~^t g_v / colmass):
       //   g_u  <- [t==T] g_u^seed - u~ (K~ cv)_i                  column VJP
       //   h    <- u~ g_u
       //   G_ik <- G_ik - u~ cv_k - h v~^{t-1}_k                    both VJPs into gK
-      //   g_v  <- -v~^{t-1} (K~' h)                                row VJP
+      //   g_v  <- -v~^{t-1} (K~' h)                                row VJP (t >= 2)
       //   u~   <- 1/(K~ v~^{t-2})_i                                replay (t >= 2)
-      for (int t = Th; t >= 1; --t) {
+      // The first level (seed g_u) and the last (t = 1: v^0 = lvi is held
+      // constant, so neither g_v nor a replay is needed) are peeled, so the
+      // steady-state body is branch-free.  Padding rows (K~ row = 0) get a
+      // finite u~ from the clamped reciprocal, hence h = 0 and no column
+      // contribution; their G is discarded in the epilogue.
+      auto level = [&](const int t, auto first_c, auto last_c) {
+        constexpr bool FIRST = decltype(first_c)::value;
+        constexpr bool LAST = decltype(last_c)::value;
         S cv[M], vp[M], c[M];
         lds_vec<S, M>(cv, vec0);
         lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
-        const S* vppp = vh + size_t(t >= 2 ? t - 2 : 0) * P;
-        const bool first = t == Th;
-        const bool replay = t >= 2;
+        const S* vppp = vh + size_t(LAST ? 0 : t - 2) * P;
   #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
   #pragma unroll
@@ -628,35 +656,42 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           S kr[M];
           lds_vec<S, M>(kr, Kt + size_t(i) * P);
           const S sig = rdot<S, M>(kr, cv);
-          S den;
-          {
+          S den = S(1);
+          if constexpr (!LAST) {
             S vpp[M];
             lds_vec<S, M>(vpp, vppp);
             den = rdot<S, M>(kr, vpp);
           }
-          S gs = S(0);
-          if (first) {
-            gs = slotB(i);
-            slotA(i) = ut[r];   // restore u~^T for the gK epilogue
-          }
-          const S h = ut[r] * (gs - ut[r] * sig);
+          const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
   #pragma unroll
           for (int k = 0; k < M; ++k) {
             A[r][k] = fma(-ut[r], cv[k], A[r][k]);
             A[r][k] = fma(-h, vp[k], A[r][k]);
-            c[k] = fma(kr[k], h, c[k]);
+            if constexpr (!LAST) c[k] = fma(kr[k], h, c[k]);
           }
-          ut[r] = masked_rcp(den, ok(r) && replay);
+          if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
-        if (t >= 2) {
+        if constexpr (!LAST) {
           cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
             const S vpk = vh[size_t(t - 1) * P + k];
             const S gv = -mul_(vpk, tot);
             vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
           });
         }
+      };
+      if (Th == 1) {
+        level(1, std::true_type{}, std::true_type{});
+      } else {
+        level(Th, std::true_type{}, std::false_type{});
+        for (int t = Th - 1; t >= 2; --t) level(t, std::false_type{}, std::false_type{});
+        level(1, std::false_type{}, std::true_type{});
       }
-      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed)
+      mark(6);
+      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed);
+      // v~^T and the exposures are reloaded here rather than held across the levels
+      S ex[M], vTe[M];
+      load_ex(ex);
+      lds_vec<S, M>(vTe, vh + size_t(Th) * P);
   #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int i = tid + r * NT;
@@ -668,15 +703,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         const S inv_imp = S(1.0 / double(imp_i));
   #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const S X = mul_(mul_(kr[k], uT), vT[k]);
+          const S X = mul_(mul_(kr[k], uT), vTe[k]);
           const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), X) : S(0);
-          gk[k] = fma(kr[k], A[r][k], W);
+          gk[k] = ok(r) ? fma(kr[k], A[r][k], W) : S(0);   // padding rows stay 0 for the forward
         }
         sts_vec<S, M>(Kt + size_t(i) * P, gk);
       }
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
     __syncthreads();
+    mark(7);
 
     // ---------------- g_C = gK * (-1/eps); Adam ascent  (solver.py:105-122) -
     const int s = a.state[ST_STEP];
@@ -781,6 +817,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     }
   }
   __syncthreads();
+  mark(8);
 
   // ======================= forward of step k =================================
   // Absorption point: beta = lvi (the warm-start column duals, so v~^0 = 1)
@@ -813,6 +850,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
     }
   }
   __syncthreads();
+  mark(9);
 forward_iterations:
   {
     S A[R][M];  // K~, register resident
@@ -846,7 +884,7 @@ forward_iterations:
         for (int r = 0; r < R; ++r) {
           const S sr = rdot<S, M>(A[r], vv);
           if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
-          ut[r] = masked_rcp(sr, ok(r));
+          ut[r] = rcp_clamped(sr);
         }
         if constexpr (TOLM) {
           rmax = warp_max(rmax);
@@ -882,6 +920,7 @@ forward_iterations:
     } else {
       iterate(std::false_type{});
     }
+    mark(10);
     if (tolm) {
       // residual of the chunk's last iteration needs one more row pass
       S vv[M];
@@ -920,6 +959,7 @@ forward_iterations:
       if (ok(r)) a.partial[size_t(u) * n + i] = acc;
     }
   }
+  mark(11);
   }
 }
 

@@ -231,6 +231,13 @@ class DeviceSolver:
         check(self.lib.nsw_solver_time_steps(self.h, int(steps), int(flush_l2), C.byref(tot), C.byref(fus)))
         return tot.value, fus.value
 
+    def phase_times(self) -> np.ndarray:
+        """Diagnostics: [U][16] global-timer stamps (ns) of the fused kernel's
+        phase boundaries in the last step (solver created with NSW_PHASE_TIMING=1)."""
+        out = np.zeros((self.U, 16), dtype=np.uint64)
+        check(self.lib.nsw_solver_phase_times(self.h, out.ctypes.data_as(C.POINTER(C.c_uint64)), self.U))
+        return out
+
     # -- state access ------------------------------------------------------------
     _FIELD_SHAPES = {
         "cost": lambda s: (s.U, s.n, s.m), "adam_m": lambda s: (s.U, s.n, s.m),
