@@ -217,6 +217,18 @@ __device__ __forceinline__ void sts_vec(S* dst, const S (&src)[M]) {
   }
 }
 
+// Asynchronous global -> shared copy of one scalar (cp.async, Ampere-style);
+// valid == false zero-fills the destination without reading the source.
+template <typename S>
+__device__ __forceinline__ void cp_async_zfill(S* smem_dst, const S* gsrc, bool valid) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;" ::"r"(d), "l"(gsrc), "n"(int(sizeof(S))),
+               "r"(valid ? int(sizeof(S)) : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -65,7 +65,6 @@ NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)
 NSW_REG(8, 64, 6)
-NSW_REG(8, 64, 7)
 NSW_REG(4, 128, 3)
 NSW_REG(8, 128, 3)
 NSW_REG(8, 256, 1)
@@ -94,7 +93,7 @@ NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(2, 128, 1)
 NSW_REG(2, 256, 1)
-NSW_REG(2, 512, 1)
+NSW_REG(4, 256, 1)   // (2, 512) at M = 32 crashes ptxas 12.9
 #endif
 #endif
 

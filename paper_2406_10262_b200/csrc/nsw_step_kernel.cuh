@@ -93,7 +93,8 @@ __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
-                      size_t(NT / 32) + 4) +
+                      size_t(NT / 32) + 4 + (sizeof(S) == 4 ? 2 * size_t(NT) * R : 0) + P) +
+         32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
          (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
 }
 
@@ -200,9 +201,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* rowB = rowA + (PAD ? 0 : size_t(NT) * R);
   S* colres = rowB + (PAD ? 0 : size_t(NT) * R);  // [2][P] column residuals (tolerance mode)
   S* redmax = colres + 2 * P;                     // [NW] per-warp row-residual maxima
+  // per-item / per-position inputs staged once per launch (the seed, the gK
+  // epilogue and the impact terms read them from here, not from global)
+  S* relS = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(redmax + NW) + 15) & ~uintptr_t(15));  // [NT*R] relevance (0 on padding rows)
+  S* impS = relS + (sizeof(S) == 4 ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
+  constexpr bool STAGE = sizeof(S) == 4;          // fp64 tiles keep their shared memory for rows
+  S* exS = impS + (STAGE ? size_t(NT) * R : 0);   // [P] exposures (0 from column m-1 on)
+  double* exD = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(exS + P) + 15) & ~uintptr_t(15));  // [P]
   // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
   unsigned char* tc_base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(redmax + NW + 4) + 127) & ~uintptr_t(127));
+      (reinterpret_cast<uintptr_t>(exD + P) + 127) & ~uintptr_t(127));
   float* Bop = reinterpret_cast<float*>(tc_base);            // [2][2][16 x 8]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tc_base + 2048);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_base + 2056);
@@ -259,13 +267,40 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
   auto inv_mass = [&](int k) -> S { return k == m - 1 ? a.inv_mass_dummy : S(1); };
   // gx = r e / Imp (solver.py:86-89); fp32 uses a per-row reciprocal
-  auto gx_of = [&](S rr, S e, S imp_i, S inv_imp) -> S {
-    if constexpr (sizeof(S) == 4) return mul_(mul_(rr, e), inv_imp);
-    else return F::div(mul_(rr, e), imp_i);
+  // (impv = impv_of(i): 1/Imp_i on the fp32 path, Imp_i on the fp64 path)
+  auto gx_of = [&](S rr, S e, S impv) -> S {
+    if constexpr (sizeof(S) == 4) return mul_(mul_(rr, e), impv);
+    else return F::div(mul_(rr, e), impv);
   };
 
-  // warm L2 with this user's tiles (C, Adam moments, duals, history,
-  // relevance): one prefetch per 128-byte line, spread over the CTA.
+  const bool rebuild = phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING || phase == PHASE_FWD_CONT ||
+                       phase == PHASE_FWD_FIN;
+  // All of this launch's small per-user inputs are requested up front, so
+  // their latencies overlap: the v~ history goes global -> shared memory
+  // asynchronously (cp.async, zero-filled past column m-1); alpha, beta,
+  // relevance and Imp go through registers and are stored after the tile is
+  // zeroed.
+  if (rebuild) {
+    for (int idx = tid; idx < (Th + 1) * P; idx += NT) {
+      const int t = idx / P, k = idx - t * P;
+      cp_async_zfill(vh + idx, hu + size_t(t) * m + (k < m ? k : 0), k < m);
+    }
+  }
+  cp_async_commit();
+  S al[R], rv[R];
+  double iv[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * NT;
+    al[r] = (rebuild && i < n) ? a.alpha[size_t(u) * n + i] : S(0);
+    if constexpr (STAGE) {
+      rv[r] = i < n ? relu[i] : S(0);
+      iv[r] = i < n ? a.imp[i] : 1.0;
+    }
+  }
+  const S bt0 = (rebuild && tid < m) ? a.beta[size_t(u) * m + tid] : S(0);
+  // warm L2 with this user's big tiles (C, Adam moments): one prefetch per
+  // 128-byte line, spread over the CTA.
   {
     auto pf = [&](const void* base, size_t bytes) {
       const char* b = reinterpret_cast<const char*>(base);
@@ -277,43 +312,45 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       pf(mu, size_t(nm) * sizeof(S));
       pf(vu, size_t(nm) * sizeof(S));
     }
-    pf(hu, size_t(T + 1) * m * sizeof(S));
-    pf(a.alpha + size_t(u) * n, size_t(n) * sizeof(S));
-    pf(relu, size_t(n) * sizeof(S));
   }
   // zero the tile (padding rows / columns must stay 0) and the small vectors
   for (int q = tid; q < NT * R * P / V; q += NT) reinterpret_cast<V16<S>*>(Kt)[q].v = V16<S>{}.v;
   if (tid < P) {
     vec0[tid] = S(0);
-    vec1[tid] = S(0);
+    vec1[tid] = bt0;
     vec2[tid] = S(0);
+    exS[tid] = tid < m - 1 ? a.expo[tid < m - 1 ? tid : 0] : S(0);
+    exD[tid] = tid < m - 1 ? a.expo_d[tid < m - 1 ? tid : 0] : 0.0;
   }
-  // exposures, loaded where used so they are not live across the loops
-  auto load_ex = [&](S (&e)[M]) {
-#pragma unroll
-    for (int k = 0; k < M; ++k) e[k] = (k < m - 1) ? a.expo[(k < m - 1) ? k : 0] : S(0);
-  };
   __syncthreads();
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = tid + r * NT;
+    if (rebuild) slotA(i) = al[r];
+    if constexpr (STAGE) {
+      relS[i] = rv[r];
+      impS[i] = S(1.0 / iv[r]);   // reciprocal: gx is two multiplies
+    }
+  }
+  // relevance and Imp (fp32: 1/Imp) of item i; fp64 reads them from global
+  // and divides by Imp in the reference's order
+  auto rel_of = [&](int i) -> S {
+    if constexpr (STAGE) return relS[i];
+    else return i < n ? relu[i] : S(0);
+  };
+  auto impv_of = [&](int i) -> S {
+    if constexpr (STAGE) return impS[i];
+    else return i < n ? S(a.imp[i]) : S(1);
+  };
+  // exposures, loaded where used so they are not live across the loops
+  auto load_ex = [&](S (&e)[M]) { lds_vec<S, M>(e, exS); };
+  cp_async_wait_all();
+  __syncthreads();
+  mark(1);
 
-  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING || phase == PHASE_FWD_CONT || phase == PHASE_FWD_FIN) {
+  if (rebuild) {
     // ---------------- rebuild K~ from C, alpha, beta (step k-1's for the
     // backward; this step's for a tolerance-mode continuation / finish) ------
-    if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
-    for (int i = tid; i < n; i += NT) slotA(i) = a.alpha[size_t(u) * n + i];
-    for (int idx0 = tid; idx0 < (Th + 1) * P; idx0 += 8 * NT) {
-      S hv[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int idx = idx0 + j * NT;
-        const int t = idx / P, k = idx - t * P;
-        hv[j] = (idx < (Th + 1) * P && k < m) ? hu[size_t(t) * m + k] : S(0);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (idx0 + j * NT < (Th + 1) * P) vh[idx0 + j * NT] = hv[j];
-    }
-    __syncthreads();
-    mark(1);
     if (vec_ok) {
       const int nq = nm / V;
       for (int q0 = tid; q0 < nq; q0 += 8 * NT) {
@@ -386,11 +423,11 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
         const S uT = slotA(i);
-        const double rr = double(relu[i]);
+        const double rr = double(rel_of(i));
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < M; ++k)
-          if (k < m - 1) acc = fma(rr * a.expo_d[(k < m - 1) ? k : 0], double(mul_(mul_(kr[k], uT), vT[k])), acc);
+          if (k < m - 1) acc = fma(rr * exD[k], double(mul_(mul_(kr[k], uT), vT[k])), acc);
         a.partial[size_t(u) * n + i] = acc;
       }
       return;
@@ -445,14 +482,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           const int i = tid + r * NT;
           lds_vec<S, M>(Kr[r], Kt + size_t(i) * P);
           ut[r] = slotA(i);
-          const S rr = ok(r) ? relu[i] : S(0);
-          const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
-          const S inv_imp = S(1.0 / double(imp_i));
+          const S rr = rel_of(i);
           S gsum = S(0);
 #pragma unroll
           for (int k = 0; k < M; ++k) {
             if (k < m - 1) {
-              const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), mul_(mul_(Kr[r][k], ut[r]), vT[k]));
+              const S W = mul_(gx_of(rr, ex[k], impv_of(i)), mul_(mul_(Kr[r][k], ut[r]), vT[k]));
               gsum += W;
               c[k] += W;
             }
@@ -577,12 +612,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         S gk[M];
         const S uT = slotA(i);
-        const S rr = ok(r) ? relu[i] : S(0);
-        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
-        const S inv_imp = S(1.0 / double(imp_i));
+        const S rr = rel_of(i);
 #pragma unroll
         for (int k = 0; k < M; ++k) {
-          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), mul_(mul_(Kr[r][k], uT), vT[k])) : S(0);
+          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], impv_of(i)), mul_(mul_(Kr[r][k], uT), vT[k])) : S(0);
           gk[k] = fma(Kr[r][k], S(g16[k]), W);
         }
         sts_vec<S, M>(Kt + size_t(i) * P, gk);
@@ -608,16 +641,14 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           S kr[M];
           lds_vec<S, M>(kr, Kt + size_t(i) * P);
           ut[r] = slotA(i);
-          const S rr = ok(r) ? relu[i] : S(0);
-          const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
-          const S inv_imp = S(1.0 / double(imp_i));
+          const S rr = rel_of(i);
           S gsum = S(0);
   #pragma unroll
           for (int k = 0; k < M; ++k) {
             A[r][k] = S(0);
             if (k < m - 1) {
               const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
-              const S W = mul_(gx_of(rr, ex[k], imp_i, inv_imp), X);
+              const S W = mul_(gx_of(rr, ex[k], impv_of(i)), X);
               gsum += W;
               c[k] += W;
             }
@@ -698,13 +729,11 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         S kr[M], gk[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
         const S uT = slotA(i);
-        const S rr = ok(r) ? relu[i] : S(0);
-        const S imp_i = ok(r) ? S(a.imp[i]) : S(1);
-        const S inv_imp = S(1.0 / double(imp_i));
+        const S rr = rel_of(i);
   #pragma unroll
         for (int k = 0; k < M; ++k) {
           const S X = mul_(mul_(kr[k], uT), vTe[k]);
-          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], imp_i, inv_imp), X) : S(0);
+          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], impv_of(i)), X) : S(0);
           gk[k] = ok(r) ? fma(kr[k], A[r][k], W) : S(0);   // padding rows stay 0 for the forward
         }
         sts_vec<S, M>(Kt + size_t(i) * P, gk);
@@ -947,13 +976,13 @@ forward_iterations:
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const int i = tid + r * NT;
-      const double rr = ok(r) ? double(relu[i]) : 0.0;
+      const double rr = double(rel_of(i));
       double acc = 0.0;
 #pragma unroll
       for (int k = 0; k < M; ++k) {
         if (k < m - 1) {
           const S X = mul_(mul_(A[r][k], ut[r]), vv[k]);
-          acc = fma(rr * a.expo_d[(k < m - 1) ? k : 0], double(X), acc);
+          acc = fma(rr * exD[k], double(X), acc);
         }
       }
       if (ok(r)) a.partial[size_t(u) * n + i] = acc;
