@@ -149,7 +149,10 @@ template <typename S, int M, int NT, class Op, class Fin>
 __device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fin) {
   constexpr int NW = NT / 32;
   constexpr int CF = (M + 31) / 32;
-  const int lane = threadIdx.x & 31;
+  // lane id re-read per reduction (volatile: not hoisted out of the hot
+  // loops, where a loop-invariant copy would only be spilled)
+  int lane;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
   const int warp = threadIdx.x >> 5;
   int base = 0, lim = M;
   reduce_scatter<S, M, M, 16, Op>(v, lane, base, lim);

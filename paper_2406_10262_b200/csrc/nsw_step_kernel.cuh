@@ -61,8 +61,17 @@ __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a,
 // Row dot product with two interleaved accumulators (halves the dependent
 // FMA chain).  Every place that forms u~ = 1/(K~ v~) uses this one function,
 // so the forward and the backward's replay produce bit-identical u~.
-template <typename S, int M>
+// CH = 2: two interleaved FMA chains (short latency for tiles with few rows
+// per thread); CH = 1: one chain (tiles with >= 4 independent rows per thread
+// have ILP to spare, and the chains' final add is saved).
+template <typename S, int M, int CH = 2>
 __device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
+  if constexpr (CH == 1) {
+    S s0 = S(0);
+#pragma unroll
+    for (int k = 0; k < M; ++k) s0 = fma(x[k], y[k], s0);
+    return s0;
+  }
   S s0 = S(0), s1 = S(0);
 #pragma unroll
   for (int k = 0; k + 1 < M; k += 2) {
@@ -188,6 +197,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   constexpr bool PAD = RowSlots<S, M>::kPad;
   constexpr int NW = NT / 32;
   constexpr int V = 16 / sizeof(S);
+  constexpr int CH = R >= 4 ? 1 : 2;   // row-dot chains; one value for every u~ (forward, replay, u~^T)
   static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (int i = tid; i < NT * R; i += NT) {
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        slotA(i) = i < n ? F::rcp_fast(rdot<S, M>(kr, vT1)) : S(0);   // u~^T
+        slotA(i) = i < n ? F::rcp_fast(rdot<S, M, CH>(kr, vT1)) : S(0);   // u~^T
       }
     }
     const int improved = a.state[ST_IMPROVED];
@@ -525,8 +535,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int i = tid + r * NT;
-          const S sig = rdot<S, M>(Kr[r], cv);
-          const S den = rdot<S, M>(Kr[r], vpp);
+          const S sig = rdot<S, M, CH>(Kr[r], cv);
+          const S den = rdot<S, M, CH>(Kr[r], vpp);
           S gs = S(0);
           if (first) {
             gs = slotB(i);
@@ -686,12 +696,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           const int i = tid + r * NT;
           S kr[M];
           lds_vec<S, M>(kr, Kt + size_t(i) * P);
-          const S sig = rdot<S, M>(kr, cv);
+          const S sig = rdot<S, M, CH>(kr, cv);
           S den = S(1);
           if constexpr (!LAST) {
             S vpp[M];
             lds_vec<S, M>(vpp, vppp);
-            den = rdot<S, M>(kr, vpp);
+            den = rdot<S, M, CH>(kr, vpp);
           }
           const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
   #pragma unroll
@@ -911,7 +921,7 @@ forward_iterations:
         S rmax = S(0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const S sr = rdot<S, M>(A[r], vv);
+          const S sr = rdot<S, M, CH>(A[r], vv);
           if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
           ut[r] = rcp_clamped(sr);
         }
@@ -957,7 +967,7 @@ forward_iterations:
       S rmax = S(0);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M>(A[r], vv) - S(1)));
+        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M, CH>(A[r], vv) - S(1)));
       rmax = warp_max(rmax);
       if (lane == 0) redmax[warp] = rmax;
       __syncthreads();
