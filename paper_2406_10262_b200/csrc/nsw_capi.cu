@@ -74,6 +74,9 @@ const Variant* choose_variant(int dtype, int n, int m, int T, int forced) {
     if (a->M != b->M) return a->M < b->M;
     if (a->CL != b->CL) return a->CL < b->CL;
     if (a->rows != b->rows) return a->rows < b->rows;
+    // one-warp tiles (NT = 32: 7 single-wave CTAs per SM, but less latency
+    // hiding and slower once-per-step phases) only by explicit choice
+    if ((a->NT >= 64) != (b->NT >= 64)) return a->NT >= 64;
     if (a->R != b->R) return a->R > b->R;
     return a->minb < b->minb;
   });
@@ -349,6 +352,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is single-GPU only (the lock-step test is not exchanged)");
   const int T = config->sinkhorn_max_iters;
   const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
+  if (const char* e = std::getenv("NSW_MAIN_TILE"); e && var && var->CL == 1) {   // experiments: "R,NT"
+    int r = 0, nt = 0;
+    if (std::sscanf(e, "%d,%d", &r, &nt) == 2)
+      for (auto& v : variant_registry())
+        if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n) var = &v;
+  }
   if (!var)
     return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +
                                          " n=" + std::to_string(n) + " m=" + std::to_string(m) +
@@ -437,6 +446,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);
     const Variant* wide = choose_wide_variant(var, n, T);
+    if (const char* e = std::getenv("NSW_TAIL_TILE")) {   // experiments: "R,NT" of the tail tile
+      int r = 0, nt = 0;
+      if (std::sscanf(e, "%d,%d", &r, &nt) == 2)
+        for (auto& v : variant_registry())
+          if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n) wide = &v;
+    }
     const int slots = per_sm * sms;
     if (wide && wide != var && slots > 0) {
       const int rem = users_local % slots;

@@ -156,6 +156,19 @@ __device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fi
   const int warp = threadIdx.x >> 5;
   int base = 0, lim = M;
   reduce_scatter<S, M, M, 16, Op>(v, lane, base, lim);
+  if constexpr (NW == 1) {
+    // one-warp CTA: the owning lane finishes its column; warp barriers order
+    // fin's shared-memory writes after every lane's reads of the previous
+    // values and publish them
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < CF; ++j) {
+      const int col = base + j;
+      if (col < lim && col < m) fin(col, v[j]);
+    }
+    __syncwarp();
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < CF; ++j) {
     const int col = base + j;
@@ -191,6 +204,35 @@ __device__ __forceinline__ void lds_vec(S (&dst)[M], const S* src) {
       const double2 t = reinterpret_cast<const double2*>(src)[q];
       if (2 * q + 0 < M) dst[(2 * q + 0 < M) ? 2 * q + 0 : 0] = t.x;
       if (2 * q + 1 < M) dst[(2 * q + 1 < M) ? 2 * q + 1 : 0] = t.y;
+    }
+  }
+}
+
+// Same, through volatile shared loads: re-read at every use instead of being
+// kept live in registers (for register-lean loops that fetch a broadcast
+// vector once per row).
+template <typename S, int M>
+__device__ __forceinline__ void lds_vec_nc(S (&dst)[M], const S* src) {
+  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(src));
+  if constexpr (sizeof(S) == 4) {
+#pragma unroll
+    for (int q = 0; q < (M + 3) / 4; ++q) {
+      float x, y, z, w;
+      asm volatile("ld.volatile.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(x), "=f"(y), "=f"(z), "=f"(w)
+                   : "r"(a + 16 * q));
+      if (4 * q + 0 < M) dst[(4 * q + 0 < M) ? 4 * q + 0 : 0] = x;
+      if (4 * q + 1 < M) dst[(4 * q + 1 < M) ? 4 * q + 1 : 0] = y;
+      if (4 * q + 2 < M) dst[(4 * q + 2 < M) ? 4 * q + 2 : 0] = z;
+      if (4 * q + 3 < M) dst[(4 * q + 3 < M) ? 4 * q + 3 : 0] = w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < (M + 1) / 2; ++q) {
+      double x, y;
+      asm volatile("ld.volatile.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a + 16 * q));
+      if (2 * q + 0 < M) dst[(2 * q + 0 < M) ? 2 * q + 0 : 0] = x;
+      if (2 * q + 1 < M) dst[(2 * q + 1 < M) ? 2 * q + 1 : 0] = y;
     }
   }
 }

@@ -61,6 +61,7 @@ NSW_REG(2, 512, 1)
 #else
 #if NSW_M <= 11
 NSW_REG_TC(4, 128, 4)
+NSW_REG(16, 32, 7)   // one-warp tile, 7 per SM: 1036 users per wave (config 1 in one wave)
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)

@@ -102,7 +102,7 @@ __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
-                      size_t(NT / 32) + 4 + (sizeof(S) == 4 ? 2 * size_t(NT) * R : 0) + P) +
+                      size_t(NT / 32) + 4 + (sizeof(S) == 4 && NT >= 64 ? 2 * size_t(NT) * R : 0) + P) +
          32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
          (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
 }
@@ -198,6 +198,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   constexpr int NW = NT / 32;
   constexpr int V = 16 / sizeof(S);
   constexpr int CH = R >= 4 ? 1 : 2;   // row-dot chains; one value for every u~ (forward, replay, u~^T)
+  // register-lean backward (tiles packed 7 per SM): the v~ history rows are
+  // re-read from shared memory per row instead of held across the row loop
+  constexpr bool LEAN = MINB >= 7;
   static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
@@ -214,8 +217,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // per-item / per-position inputs staged once per launch (the seed, the gK
   // epilogue and the impact terms read them from here, not from global)
   S* relS = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(redmax + NW) + 15) & ~uintptr_t(15));  // [NT*R] relevance (0 on padding rows)
-  S* impS = relS + (sizeof(S) == 4 ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
-  constexpr bool STAGE = sizeof(S) == 4;          // fp64 tiles keep their shared memory for rows
+  S* impS = relS + (sizeof(S) == 4 && NT >= 64 ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
+  constexpr bool STAGE = sizeof(S) == 4 && NT >= 64;   // fp64 / 1-warp tiles keep their shared memory for rows
   S* exS = impS + (STAGE ? size_t(NT) * R : 0);   // [P] exposures (0 from column m-1 on)
   double* exD = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(exS + P) + 15) & ~uintptr_t(15));  // [P]
   // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
@@ -350,6 +353,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   };
   auto impv_of = [&](int i) -> S {
     if constexpr (STAGE) return impS[i];
+    else if constexpr (sizeof(S) == 4) return i < n ? F::rcp_fast(S(a.imp[i])) : S(1);
     else return i < n ? S(a.imp[i]) : S(1);
   };
   // exposures, loaded where used so they are not live across the loops
@@ -687,7 +691,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         constexpr bool LAST = decltype(last_c)::value;
         S cv[M], vp[M], c[M];
         lds_vec<S, M>(cv, vec0);
-        lds_vec<S, M>(vp, vh + size_t(t - 1) * P);
+        const S* vpp1 = vh + size_t(t - 1) * P;
+        if constexpr (!LEAN) lds_vec<S, M>(vp, vpp1);
         const S* vppp = vh + size_t(LAST ? 0 : t - 2) * P;
   #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
@@ -700,10 +705,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           S den = S(1);
           if constexpr (!LAST) {
             S vpp[M];
-            lds_vec<S, M>(vpp, vppp);
+            if constexpr (LEAN) lds_vec_nc<S, M>(vpp, vppp);
+            else lds_vec<S, M>(vpp, vppp);
             den = rdot<S, M, CH>(kr, vpp);
           }
           const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
+          if constexpr (LEAN) lds_vec_nc<S, M>(vp, vpp1);
   #pragma unroll
           for (int k = 0; k < M; ++k) {
             A[r][k] = fma(-ut[r], cv[k], A[r][k]);
