@@ -132,6 +132,11 @@ nsw_status nsw_solver_status(nsw_solver* s, int32_t* phase, int32_t* steps, int3
 nsw_status nsw_solver_stream(nsw_solver* s, void** stream);
 /* Best policy [users_local][n][m] float64 and the trace (host). */
 nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace);
+/* Top-m ranking of the returned (best-F) policy, computed on the device:
+ * out_host[u][k] = argmax_i X[u][i][k] for k < m-1, lowest index on ties
+ * ([U][m-1] int32).  The reference has no ranking extraction; this is the
+ * definition of SURVEY.md 8(a) (numpy argmax over items). */
+nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host);
 
 /* Raw state access for tests and one-step parity (host float64 buffers):
  * field = "cost" | "adam_m" | "adam_v" [U][n][m], "alpha" [U][n], "beta" [U][m],
@@ -154,6 +159,11 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
  * boundaries, [count users][16], of the last step the solver ran.  Only when
  * the environment had NSW_PHASE_TIMING=1 at nsw_solver_create. */
 nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count);
+
+/* Top-m ranking of a device policy tensor X [U][n][m] (float32 / float64)
+ * into device int32 out [U][m-1], on `stream` (cudaStream_t, 0 = default). */
+nsw_status nsw_top_positions_f32(const float* X, int32_t U, int32_t n, int32_t m, int32_t* out, void* stream);
+nsw_status nsw_top_positions_f64(const double* X, int32_t U, int32_t n, int32_t m, int32_t* out, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * 3. Inner operator seam (device pointers, fixed schedule).                *

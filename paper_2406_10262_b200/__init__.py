@@ -14,6 +14,7 @@ _EXPORTS = {
     "solver": ("SolveTrace", "DeviceOptions", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError"),
     "data": ("exposure_model", "make_instance", "BASELINE_CONFIGS"),
     "sinkhorn": ("sinkhorn_batch", "sinkhorn_backward_batch"),
+    "ranking": ("top_positions",),
     "distributed": ("solve_fair_ranking_distributed", "shard_users"),
 }
 

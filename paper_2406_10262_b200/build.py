@@ -54,7 +54,7 @@ def _jobs():
     for f64 in (0, 1):
         jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(BUILD, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
                      [f"-DNSW_F64={f64}"]))
-    for name in ("nsw_common", "nsw_capi", "nsw_ops"):
+    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank"):
         jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(BUILD, name + ".o"), []))
     return jobs
 

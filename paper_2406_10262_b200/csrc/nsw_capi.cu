@@ -828,6 +828,24 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
   return NSW_OK;
 }
 
+nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host) {
+  if (!s || !out_host) return fail(NSW_ERR_ARG, "NULL argument");
+  int32_t* d = nullptr;
+  const size_t count = size_t(s->U) * (s->m - 1);
+  CUDA_TRY(cudaMalloc(&d, count * sizeof(int32_t)));
+  nsw_status e = s->dtype == NSW_F64
+                     ? nsw_top_positions_f64((const double*)s->xbest, s->U, s->n, s->m, d, s->stream)
+                     : nsw_top_positions_f32((const float*)s->xbest, s->U, s->n, s->m, d, s->stream);
+  if (e == NSW_OK) {
+    s->launches += 1;
+    if (cudaMemcpyAsync(out_host, d, count * sizeof(int32_t), cudaMemcpyDeviceToHost, s->stream) != cudaSuccess ||
+        cudaStreamSynchronize(s->stream) != cudaSuccess)
+      e = fail(NSW_ERR_CUDA, "top_positions copy failed");
+  }
+  cudaFree(d);
+  return e;
+}
+
 nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count) {
   if (!s || !out) return fail(NSW_ERR_ARG, "NULL argument");
   if (!s->phase_ns) return fail(NSW_ERR_UNSUPPORTED, "phase timing is off (set NSW_PHASE_TIMING=1 before creating the solver)");

@@ -260,6 +260,13 @@ class DeviceSolver:
     def set_scalar(self, name: str, value: int) -> None:
         check(self.lib.nsw_solver_set_scalar(self.h, name.encode(), int(value)), f"set {name}")
 
+    def top_positions(self) -> np.ndarray:
+        """Top-m ranking of the best policy, computed on the device:
+        int32 [U][m-1], argmax over items per real position (lowest index on ties)."""
+        out = np.empty((self.U, self.m - 1), dtype=np.int32)
+        check(self.lib.nsw_solver_top_positions(self.h, out.ctypes.data_as(C.POINTER(C.c_int32))), "top_positions")
+        return out
+
     def result(self):
         """(best policy float64 [U][n][m], SolveTrace)."""
         J = self.config.outer_max_iters
