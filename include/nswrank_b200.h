@@ -111,9 +111,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
                              nsw_solver** out);
 nsw_status nsw_solver_destroy(nsw_solver* s);
 
-/* Device pointers of the impact exchange: local [n] float64 (written by
- * nsw_solver_local_step), gathered [world][n] float64 (read by
- * nsw_solver_finalize).  May be rebound to caller-owned device buffers. */
+/* Device pointers of the impact exchange: local [n + 1] float64 (written by
+ * nsw_solver_local_step: the n item impacts, then -- tolerance schedule --
+ * this shard's count of converged users), gathered [world][n + 1] float64
+ * (read by nsw_solver_finalize).  May be rebound to caller-owned buffers. */
 nsw_status nsw_solver_exchange_buffers(nsw_solver* s, void** local_dev, void** gathered_dev);
 nsw_status nsw_solver_bind_exchange(nsw_solver* s, void* local_dev, void* gathered_dev);
 
@@ -123,6 +124,18 @@ nsw_status nsw_solver_local_step(nsw_solver* s, void* stream);
 /* Objective, gradient norm, best-iterate and stop decisions from the
  * gathered impacts (solver.py:206-223).  No-op once finished. */
 nsw_status nsw_solver_finalize(nsw_solver* s, void* stream);
+/* Tolerance schedule across shards (sinkhorn.py:237-246 over all users):
+ * after each forward chunk, nsw_solver_tol_local writes this shard's
+ * per-iteration residual maxima [tol_chunk] float64 into the bound buffer;
+ * the caller all-reduces it (MAX, in place); nsw_solver_tol_decide picks t*
+ * and returns the device phase (host-synchronising): 5 = next chunk (call
+ * nsw_solver_local_step again), 6 = t* found (call nsw_solver_local_step for
+ * the finish launch), anything else = no forward pending.  Pass the total
+ * user count with nsw_solver_set_scalar(s, "users_total", U) so the
+ * SolverError fraction (solver.py:200-205) is over all ranks. */
+nsw_status nsw_solver_bind_tol_exchange(nsw_solver* s, void* cmax_dev);
+nsw_status nsw_solver_tol_local(nsw_solver* s, void* stream);
+nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase);
 /* local_step + finalize, world must be 1; uses the solver's own stream and
  * CUDA graph.  Runs at most max_steps outer steps; *done = 1 when finished. */
 nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done);

@@ -130,8 +130,11 @@ struct nsw_solver {
   int tol = 0;             // tolerance-mode schedule
   int* state_host = nullptr;  // pinned
   bool own_exchange = true;
-  double* own_imp_local = nullptr;
-  double* own_imp_all = nullptr;
+  double* own_imp_local = nullptr;   // [n + 1]
+  double* own_imp_all = nullptr;     // [world][n + 1]
+  double* own_tol = nullptr;         // [chunk] per-iteration residual maxima (tolerance mode)
+  double* tolbuf = nullptr;          // bound exchange buffer for them (all-reduce MAX in place)
+  int U_total = 0;                   // users over all ranks
   cudaStream_t stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
@@ -263,7 +266,8 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
 nsw_status launch_impact_reduce(nsw_solver* s, cudaStream_t st) {
   const dim3 grid((s->n + IMP_ITEMS - 1) / IMP_ITEMS, s->imp_chunks);
   impact_reduce_kernel<<<grid, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n, s->imp_chunks, s->split, s->counter,
-                                                     s->imp_local, s->state, s->tol);
+                                                     s->imp_local, s->state, s->tol, s->res, s->T,
+                                                     s->cfg.sinkhorn_tol);
   CUDA_TRY(cudaGetLastError());
   s->launches += 1;
   return NSW_OK;
@@ -302,6 +306,7 @@ nsw_status refresh_args(nsw_solver* s) {
   s->fin.state = s->state;
   s->fin.tol_mode = s->tol;
   s->fin.U = s->U;
+  s->fin.U_total = s->U_total;
   s->fin.T = s->T;
   s->fin.tol = s->cfg.sinkhorn_tol;
   s->fin.res = s->res;
@@ -401,8 +406,8 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   // impact reduction: ~2 CTAs per SM of (8 items x user chunk)
   s->imp_chunks = std::max(1, std::min(std::min(users_local, 64), (2 * 148 * IMP_ITEMS + n - 1) / n));
   ALLOC(s->split, size_t(s->imp_chunks) * n * 8);
-  ALLOC(s->own_imp_local, size_t(n) * 8);
-  ALLOC(s->own_imp_all, size_t(world) * n * 8);
+  ALLOC(s->own_imp_local, size_t(n + 1) * 8);
+  ALLOC(s->own_imp_all, size_t(world) * (n + 1) * 8);
   ALLOC(s->imp_cur, size_t(n) * 8);
   ALLOC(s->rel_sq, size_t(n) * 8);
   ALLOC(s->best, 8);
@@ -418,7 +423,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     CUDA_TRY(cudaMemset(s->phase_ns, 0, size_t(users_local) * 16 * 8));
   }
   s->tol = options->schedule == NSW_SCHEDULE_TOLERANCE;
-  if (s->tol) ALLOC(s->res, size_t(users_local) * (T + 1) * 8);
+  if (s->tol) {
+    ALLOC(s->res, size_t(users_local) * (T + 1) * 8);
+    ALLOC(s->own_tol, size_t(std::max(1, options->tol_chunk > 0 ? options->tol_chunk : 16)) * 8);
+  }
+  s->tolbuf = s->own_tol;
+  s->U_total = users_local;
 #undef ALLOC
   s->imp_local = s->own_imp_local;
   s->imp_all = world == 1 ? s->own_imp_local : s->own_imp_all;
@@ -530,7 +540,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
-                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters, s->phase_ns};
+                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters, s->phase_ns, s->own_tol};
   for (void* p : bufs)
     if (p) cudaFree(p);
   if (s->state_host) cudaFreeHost(s->state_host);
@@ -551,6 +561,31 @@ nsw_status nsw_solver_bind_exchange(nsw_solver* s, void* local_dev, void* gather
   s->imp_local = (double*)local_dev;
   s->imp_all = (double*)gathered_dev;
   return refresh_args(s);
+}
+
+static nsw_status tol_local(nsw_solver* s, cudaStream_t st);
+static nsw_status tol_decide(nsw_solver* s, cudaStream_t st, int* phase);
+
+nsw_status nsw_solver_bind_tol_exchange(nsw_solver* s, void* cmax_dev) {
+  if (!s || !cmax_dev) return fail(NSW_ERR_ARG, "NULL argument");
+  if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
+  s->tolbuf = (double*)cmax_dev;
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_tol_local(nsw_solver* s, void* stream) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
+  return tol_local(s, stream ? (cudaStream_t)stream : s->stream);
+}
+
+nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
+  int ph = 0;
+  nsw_status e = tol_decide(s, stream ? (cudaStream_t)stream : s->stream, &ph);
+  if (phase) *phase = ph;
+  return e;
 }
 
 nsw_status nsw_solver_local_step(nsw_solver* s, void* stream) {
@@ -589,17 +624,32 @@ static nsw_status ensure_graph(nsw_solver* s) {
 // test (tol_check_kernel) finds t*; the host reads the device phase after
 // each chunk (the number of chunks is data dependent), then the finish
 // launch emits X^{t*}'s impact terms.
+static nsw_status tol_local(nsw_solver* s, cudaStream_t st) {
+  const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
+  tol_chunk_max_kernel<<<1, 256, 0, st>>>(s->res, s->U, s->T, chunk, s->state, s->tolbuf);
+  CUDA_TRY(cudaGetLastError());
+  s->launches += 1;
+  return NSW_OK;
+}
+
+static nsw_status tol_decide(nsw_solver* s, cudaStream_t st, int* phase) {
+  const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
+  tol_decide_kernel<<<1, 32, 0, st>>>(s->tolbuf, s->T, chunk, s->cfg.sinkhorn_tol, s->state);
+  CUDA_TRY(cudaGetLastError());
+  s->launches += 1;
+  CUDA_TRY(cudaMemcpyAsync(s->state_host, s->state, ST_WORDS * sizeof(int), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (phase) *phase = s->state_host[ST_PHASE];
+  return NSW_OK;
+}
+
 static nsw_status one_step_tolerance(nsw_solver* s) {
   nsw_status e = launch_fused(s, s->stream);
   if (e != NSW_OK) return e;
-  const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
   for (;;) {
-    tol_check_kernel<<<1, 256, 0, s->stream>>>(s->res, s->U, s->T, chunk, s->cfg.sinkhorn_tol, s->state);
-    CUDA_TRY(cudaGetLastError());
-    s->launches += 1;
-    e = read_state(s);
-    if (e != NSW_OK) return e;
-    const int ph = s->state_host[ST_PHASE];
+    int ph = 0;
+    if ((e = tol_local(s, s->stream)) != NSW_OK) return e;
+    if ((e = tol_decide(s, s->stream, &ph)) != NSW_OK) return e;
     if (ph == PHASE_FWD_CONT) {
       e = launch_fused(s, s->stream);
       if (e != NSW_OK) return e;
@@ -689,7 +739,7 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
     CUDA_TRY(cudaMemcpy(trace->sinkhorn_iterations, s->iters, steps * sizeof(int), cudaMemcpyDeviceToHost));
   const int err = s->state_host[ST_ERR];
   if (err & ERR_SOLVER) {
-    const double failed = 1.0 - double(s->state_host[ST_CONV]) / double(s->U);
+    const double failed = 1.0 - double(s->state_host[ST_CONV]) / double(s->U_total);
     char msg[160];
     snprintf(msg, sizeof(msg), "Sinkhorn failed to converge for %.0f%% of users within %d iterations", failed * 100.0,
              s->T);
@@ -762,6 +812,11 @@ nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value
     int v = int(value);
     CUDA_TRY(cudaMemcpy(s->state + idx, &v, 4, cudaMemcpyHostToDevice));
     return NSW_OK;
+  }
+  if (!strcmp(field, "users_total")) {   // sharded solve: users over all ranks
+    if (value < s->U) return fail(NSW_ERR_ARG, "users_total < local users");
+    s->U_total = int(value);
+    return refresh_args(s);
   }
   if (!strcmp(field, "best_is_neg_inf")) {
     const double neg_inf = -INFINITY;

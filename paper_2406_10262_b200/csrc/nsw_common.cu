@@ -22,7 +22,9 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
                                                                     int n, int chunks, double* __restrict__ split,
                                                                     unsigned int* counter,
                                                                     double* __restrict__ imp_local,
-                                                                    const int* __restrict__ state, int tol_mode) {
+                                                                    const int* __restrict__ state, int tol_mode,
+                                                                    const double* __restrict__ res, int T,
+                                                                    double tol) {
   if (!forward_ready(state[ST_PHASE], tol_mode)) return;
   constexpr int LANES = IMP_THREADS / IMP_ITEMS;
   __shared__ double red[IMP_THREADS];
@@ -61,36 +63,58 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
     for (int c = 0; c < chunks; ++c) acc += __ldcg(split + size_t(c) * n + ii);
     imp_local[ii] = acc;
   }
-  if (threadIdx.x == 0) *counter = 0u;
+  // converged = residual <= tol at the final iteration t* (sinkhorn.py:253)
+  int cnt = 0;
+  if (tol_mode) {
+    const int tstar = state[ST_TSTAR];
+    for (int u = threadIdx.x; u < U; u += IMP_THREADS) cnt += res[size_t(u) * (T + 1) + tstar] <= tol;
+  }
+  __shared__ int sc;
+  if (threadIdx.x == 0) sc = 0;
+  __syncthreads();
+  if (cnt) atomicAdd(&sc, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    imp_local[n] = double(sc);
+    *counter = 0u;
+  }
 }
 
-__global__ void __launch_bounds__(256) tol_check_kernel(const double* __restrict__ res, int U, int T, int chunk,
-                                                        double tol, int* state) {
+__global__ void __launch_bounds__(256) tol_chunk_max_kernel(const double* __restrict__ res, int U, int T,
+                                                            int chunk, const int* state, double* __restrict__ cmax) {
   const int phase = state[ST_PHASE];
   if (!(phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME || phase == PHASE_FWD_CONT)) return;
   __shared__ double red[256];
-  __shared__ int tstar;
   const int t0 = state[ST_T0];
   const int t1 = min(t0 + chunk, T);
-  if (threadIdx.x == 0) tstar = 0;
-  for (int t = t0 + 1; t <= t1; ++t) {
+  for (int j = 0; j < chunk; ++j) {
+    const int t = t0 + 1 + j;
     double mx = 0.0;
-    for (int u = threadIdx.x; u < U; u += blockDim.x) mx = fmax(mx, res[size_t(u) * (T + 1) + t]);
+    if (t <= t1)
+      for (int u = threadIdx.x; u < U; u += blockDim.x) mx = fmax(mx, res[size_t(u) * (T + 1) + t]);
     red[threadIdx.x] = mx;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
       if (threadIdx.x < w) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + w]);
       __syncthreads();
     }
-    const bool stop = red[0] <= tol;   // residual.max() <= tol (sinkhorn.py:244)
+    if (threadIdx.x == 0) cmax[j] = red[0];
     __syncthreads();
-    if (stop) {
-      if (threadIdx.x == 0) tstar = t;
+  }
+}
+
+__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state) {
+  const int phase = state[ST_PHASE];
+  if (!(phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME || phase == PHASE_FWD_CONT)) return;
+  if (threadIdx.x != 0) return;
+  const int t0 = state[ST_T0];
+  const int t1 = min(t0 + chunk, T);
+  int tstar = 0;
+  for (int t = t0 + 1; t <= t1; ++t)
+    if (cmax[t - t0 - 1] <= tol) {   // residual.max() <= tol (sinkhorn.py:244)
+      tstar = t;
       break;
     }
-  }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
   if (tstar > 0 || t1 == T) {
     state[ST_TSTAR] = tstar > 0 ? tstar : T;
     state[ST_PHASE] = PHASE_FWD_FIN;
@@ -119,17 +143,18 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
   }
   __syncthreads();
   const int tstar = f.tol_mode ? f.state[ST_TSTAR] : f.T;
-  if (f.tol_mode) {
-    // converged = residual <= tol at the final iteration (sinkhorn.py:253)
-    int cnt = 0;
-    for (int u = tid; u < f.U; u += NT) cnt += f.res[size_t(u) * (f.T + 1) + tstar] <= f.tol;
-    atomicAdd(&sConv, cnt);
+  if (f.tol_mode && tid == 0) {
+    // converged users over all ranks (each rank's count rides in slot n of
+    // its exchanged impact vector)
+    double c = 0.0;
+    for (int g = 0; g < f.world; ++g) c += f.imp_all[size_t(g) * (f.n + 1) + f.n];
+    sConv = int(c);
   }
   double accF = 0.0, accG = 0.0;
   int bad = 0;
   for (int i = tid; i < f.n; i += NT) {
     double imp = 0.0;
-    for (int g = 0; g < f.world; ++g) imp += f.imp_all[size_t(g) * f.n + i];
+    for (int g = 0; g < f.world; ++g) imp += f.imp_all[size_t(g) * (f.n + 1) + i];
     f.imp_cur[i] = imp;
     if (!(imp > 0.0) || !isfinite(imp)) bad = 1;
     accF += log(imp);
@@ -153,7 +178,7 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
     f.state[ST_T0] = 0;
     // SolverError if more than half the users missed the tolerance
     // (solver.py:200-205), checked before the impact (solver.py:206-208)
-    if (1.0 - double(sConv) / double(f.U) > 0.5) {
+    if (1.0 - double(sConv) / double(f.U_total) > 0.5) {
       f.state[ST_ERR] |= ERR_SOLVER;
       f.state[ST_PHASE] = PHASE_FINISHED;
       return;

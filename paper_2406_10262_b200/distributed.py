@@ -12,6 +12,13 @@ needs sum_u r_ui^2 over all users, exchanged once at setup.
 The exchange is torch.distributed (NCCL on GPUs, gloo in the CPU tests)
 running on the solver's own CUDA stream, captured with the step in a CUDA
 graph when the backend allows it.
+
+In the reference's tolerance schedule (sinkhorn.py:237-246) the lock-step
+stop is over ALL users: after every forward chunk the ranks all-reduce (MAX)
+their per-iteration residual maxima before the device picks t*, and each
+rank's converged-user count rides in the last slot of its exchanged impact
+vector, so the SolverError guard (solver.py:200-205) sees every user.  That
+step is host-driven (the number of chunks is data dependent), not captured.
 """
 
 from __future__ import annotations
@@ -63,12 +70,18 @@ class ShardedAscent:
         dist.all_reduce(rsq_local, group=group)
         rsq = rsq_local.cpu().numpy()
         opts = options or DeviceOptions(schedule="fixed")
+        self.tolerance = opts.schedule == "tolerance"
         self.solver = DeviceSolver(rel[self.start:self.stop], exposure.values, shape.num_items,
                                    shape.num_positions, config, opts, rel_sq_sum=rsq, world=self.world)
         n = shape.num_items
-        self.local = torch.zeros(n, dtype=torch.float64, device=dev)
-        self.gathered = torch.zeros(self.world * n, dtype=torch.float64, device=dev)
+        # impacts + this shard's converged-user count (tolerance schedule)
+        self.local = torch.zeros(n + 1, dtype=torch.float64, device=dev)
+        self.gathered = torch.zeros(self.world * (n + 1), dtype=torch.float64, device=dev)
         self.solver.bind_exchange(self.local.data_ptr(), self.gathered.data_ptr())
+        if self.tolerance:
+            self.solver.set_scalar("users_total", shape.num_users)
+            self.cmax = torch.zeros(max(1, opts.tol_chunk), dtype=torch.float64, device=dev)
+            self.solver.bind_tol_exchange(self.cmax.data_ptr())
         self.stream = torch.cuda.ExternalStream(self.solver.stream())
         self.graph = None
 
@@ -78,8 +91,28 @@ class ShardedAscent:
         self.dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
         self.solver.finalize(s)
 
+    def _tolerance_step(self):
+        s = self.stream.cuda_stream
+        self.solver.local_step(s)            # [backward + Adam +] first forward chunk
+        while True:
+            self.solver.tol_local(s)
+            self.dist.all_reduce(self.cmax, op=self.dist.ReduceOp.MAX, group=self.group)
+            phase = self.solver.tol_decide(s)
+            if phase == 5:                   # next chunk of this forward
+                self.solver.local_step(s)
+                continue
+            if phase == 6:                   # t* known: finish launch + impact terms
+                self.solver.local_step(s)
+            break
+        self.dist.all_gather_into_tensor(self.gathered, self.local, group=self.group)
+        self.solver.finalize(s)
+
     def step(self, use_graph=True):
         torch = self.torch
+        if self.tolerance:
+            with torch.cuda.stream(self.stream):
+                self._tolerance_step()
+            return
         with torch.cuda.stream(self.stream):
             if use_graph and self.graph is None:
                 try:

@@ -204,6 +204,18 @@ class DeviceSolver:
     def bind_exchange(self, local_ptr: int, gathered_ptr: int):
         check(self.lib.nsw_solver_bind_exchange(self.h, C.c_void_p(local_ptr), C.c_void_p(gathered_ptr)))
 
+    # tolerance schedule across shards (all-reduce MAX between local and decide)
+    def bind_tol_exchange(self, cmax_ptr: int):
+        check(self.lib.nsw_solver_bind_tol_exchange(self.h, C.c_void_p(cmax_ptr)), "bind_tol_exchange")
+
+    def tol_local(self, stream: int | None = None):
+        check(self.lib.nsw_solver_tol_local(self.h, C.c_void_p(stream)), "nsw_solver_tol_local")
+
+    def tol_decide(self, stream: int | None = None) -> int:
+        ph = C.c_int32()
+        check(self.lib.nsw_solver_tol_decide(self.h, C.c_void_p(stream), C.byref(ph)), "nsw_solver_tol_decide")
+        return ph.value
+
     def stream(self) -> int:
         s = C.c_void_p()
         check(self.lib.nsw_solver_stream(self.h, C.byref(s)))
