@@ -856,6 +856,11 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
     if (flush_l2) {
       flush_kernel<<<148 * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
       CUDA_TRY(cudaGetLastError());
+      // drop the flush buffer's dirty lines without writing them back: the
+      // timed step starts from a cold, clean L2 instead of paying the
+      // flush's write-backs
+      discard_kernel<<<148 * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
+      CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaEventRecord(ev[3 * i], s->stream));
     nsw_status e = launch_fused(s, s->stream);

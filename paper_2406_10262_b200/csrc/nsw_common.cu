@@ -210,4 +210,10 @@ __global__ void flush_kernel(float* buf, size_t n) {
     buf[i] = buf[i] * 0.5f + 1.0f;
 }
 
+__global__ void discard_kernel(float* buf, size_t n) {
+  // one discard per 128-byte line (n floats, 128-byte aligned buffer)
+  for (size_t l = blockIdx.x * size_t(blockDim.x) + threadIdx.x; l < n / 32; l += size_t(gridDim.x) * blockDim.x)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(buf + l * 32) : "memory");
+}
+
 }  // namespace nsw

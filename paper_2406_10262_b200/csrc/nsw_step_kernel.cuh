@@ -201,6 +201,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
   // re-read from shared memory per row instead of held across the row loop
   constexpr bool LEAN = MINB >= 7;
+  // fp32: the seed's W is folded into the adjoint as its rank-1 start value
+  constexpr bool RANK1 = sizeof(S) == 4;
   static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
@@ -657,14 +659,27 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           ut[r] = slotA(i);
           const S rr = rel_of(i);
           S gsum = S(0);
+          if constexpr (RANK1) {
+            // W = K~ .* (a b'), a_i = u~^T_i r_i / Imp_i, b_k = e_k v~^T_k:
+            // G starts at a b', so gK = K~ .* G at the end needs no W
+            const S ai = mul_(mul_(rr, impv_of(i)), ut[r]);
   #pragma unroll
-          for (int k = 0; k < M; ++k) {
-            A[r][k] = S(0);
-            if (k < m - 1) {
-              const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
-              const S W = mul_(gx_of(rr, ex[k], impv_of(i)), X);
+            for (int k = 0; k < M; ++k) {
+              A[r][k] = mul_(ai, mul_(ex[k], vT[k]));
+              const S W = mul_(kr[k], A[r][k]);
               gsum += W;
               c[k] += W;
+            }
+          } else {
+  #pragma unroll
+            for (int k = 0; k < M; ++k) {
+              A[r][k] = S(0);
+              if (k < m - 1) {
+                const S X = mul_(mul_(kr[k], ut[r]), vT[k]);
+                const S W = mul_(gx_of(rr, ex[k], impv_of(i)), X);
+                gsum += W;
+                c[k] += W;
+              }
             }
           }
           gs[r] = gsum;
@@ -735,25 +750,39 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         level(1, std::false_type{}, std::true_type{});
       }
       mark(6);
-      // gK = W + K~ .* G, written over K~ in the tile (W = gx .* X recomputed);
-      // v~^T and the exposures are reloaded here rather than held across the levels
-      S ex[M], vTe[M];
-      load_ex(ex);
-      lds_vec<S, M>(vTe, vh + size_t(Th) * P);
+      // gK = W + K~ .* G, written over K~ in the tile (fp64: W = gx .* X
+      // recomputed in the reference's operation order; fp32: folded into G
+      // at the seed).  v~^T and the exposures are reloaded here rather than
+      // held across the levels.
+      if constexpr (RANK1) {
   #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = tid + r * NT;
-        S kr[M], gk[M];
-        lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        const S uT = slotA(i);
-        const S rr = rel_of(i);
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          S kr[M], gk[M];
+          lds_vec<S, M>(kr, Kt + size_t(i) * P);
   #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          const S X = mul_(mul_(kr[k], uT), vTe[k]);
-          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], impv_of(i)), X) : S(0);
-          gk[k] = ok(r) ? fma(kr[k], A[r][k], W) : S(0);   // padding rows stay 0 for the forward
+          for (int k = 0; k < M; ++k) gk[k] = ok(r) ? mul_(kr[k], A[r][k]) : S(0);   // padding rows stay 0
+          sts_vec<S, M>(Kt + size_t(i) * P, gk);
         }
-        sts_vec<S, M>(Kt + size_t(i) * P, gk);
+      } else {
+        S ex[M], vTe[M];
+        load_ex(ex);
+        lds_vec<S, M>(vTe, vh + size_t(Th) * P);
+  #pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          S kr[M], gk[M];
+          lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          const S uT = slotA(i);
+          const S rr = rel_of(i);
+  #pragma unroll
+          for (int k = 0; k < M; ++k) {
+            const S X = mul_(mul_(kr[k], uT), vTe[k]);
+            const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], impv_of(i)), X) : S(0);
+            gk[k] = ok(r) ? fma(kr[k], A[r][k], W) : S(0);   // padding rows stay 0 for the forward
+          }
+          sts_vec<S, M>(Kt + size_t(i) * P, gk);
+        }
       }
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
@@ -1056,5 +1085,6 @@ struct FinalizeArgs {
 __global__ void finalize_kernel(FinalizeArgs f);
 __global__ void stamp_kernel(unsigned long long* stamp);
 __global__ void flush_kernel(float* buf, size_t n);
+__global__ void discard_kernel(float* buf, size_t n);
 
 }  // namespace nsw
