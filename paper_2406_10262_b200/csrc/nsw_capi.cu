@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -203,14 +204,28 @@ nsw_status upload_converted(void* dst, const double* src, size_t count) {
   return NSW_OK;
 }
 
-nsw_status download_converted(int dtype, const void* src, double* dst, size_t count) {
+nsw_status download_converted(int dtype, const void* src, double* dst, size_t count, cudaStream_t st,
+                              bool* nonfinite = nullptr) {
   if (dtype == NSW_F64) {
-    CUDA_TRY(cudaMemcpy(dst, src, count * 8, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpyAsync(dst, src, count * 8, cudaMemcpyDeviceToHost, st));
   } else {
-    std::vector<float> tmp(count);
-    CUDA_TRY(cudaMemcpy(tmp.data(), src, count * 4, cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < count; ++i) dst[i] = double(tmp[i]);
+    // widen on the device, then one copy straight into the caller's buffer
+    double* wide = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&wide, count * 8 + 16, st));
+    unsigned* bad = reinterpret_cast<unsigned*>(wide + count);   // one word past the values
+    CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
+    widen_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const float*>(src), wide, count, bad);
+    cudaError_t ce = cudaGetLastError();
+    unsigned bad_h = 0;
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(dst, wide, count * 8, cudaMemcpyDeviceToHost, st);
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&bad_h, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+    cudaFreeAsync(wide, st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+    if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("download: ") + cudaGetErrorString(ce));
+    if (nonfinite) *nonfinite = bad_h != 0;
+    return NSW_OK;
   }
+  CUDA_TRY(cudaStreamSynchronize(st));
   return NSW_OK;
 }
 
@@ -322,9 +337,47 @@ nsw_status read_state(nsw_solver* s) {
 }
 
 template <typename T>
-nsw_status dmalloc(T** p, size_t bytes) {
-  CUDA_TRY(cudaMalloc((void**)p, std::max<size_t>(bytes, 16)));
-  CUDA_TRY(cudaMemset(*p, 0, std::max<size_t>(bytes, 16)));
+nsw_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
+  // stream-ordered allocation from the device's default pool, which keeps
+  // its memory across solvers (release threshold raised once per device):
+  // a repeated solve of the same size allocates without OS calls
+  CUDA_TRY(cudaMallocAsync((void**)p, std::max<size_t>(bytes, 16), st));
+  CUDA_TRY(cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), st));
+  return NSW_OK;
+}
+
+// Pinned state words: a process-wide free list (cudaMallocHost costs
+// milliseconds; solvers come and go per solve call).
+std::mutex g_pinned_mu;
+std::vector<int*> g_pinned_free;
+
+int* pinned_state_get() {
+  {
+    std::lock_guard<std::mutex> lk(g_pinned_mu);
+    if (!g_pinned_free.empty()) {
+      int* p = g_pinned_free.back();
+      g_pinned_free.pop_back();
+      return p;
+    }
+  }
+  int* p = nullptr;
+  return cudaMallocHost((void**)&p, 64) == cudaSuccess ? p : nullptr;
+}
+
+void pinned_state_put(int* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_mu);
+  g_pinned_free.push_back(p);
+}
+
+nsw_status keep_pool_memory(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return NSW_OK;
+  cudaMemPool_t pool;
+  CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t keep = ~uint64_t(0);
+  CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  done[device] = true;
   return NSW_OK;
 }
 
@@ -353,8 +406,6 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   if (options->dtype != NSW_F32 && options->dtype != NSW_F64) return fail(NSW_ERR_ARG, "bad dtype");
   if (options->schedule != NSW_SCHEDULE_FIXED && options->schedule != NSW_SCHEDULE_TOLERANCE)
     return fail(NSW_ERR_ARG, "bad schedule");
-  if (options->schedule == NSW_SCHEDULE_TOLERANCE && world != 1)
-    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is single-GPU only (the lock-step test is not exchanged)");
   const int T = config->sinkhorn_max_iters;
   const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
   if (const char* e = std::getenv("NSW_MAIN_TILE"); e && var && var->CL == 1) {   // experiments: "R,NT"
@@ -368,7 +419,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
                                          " n=" + std::to_string(n) + " m=" + std::to_string(m) +
                                          " T=" + std::to_string(T));
   CUDA_TRY(cudaSetDevice(options->device));
+  if (nsw_status pe = keep_pool_memory(options->device); pe != NSW_OK) return pe;
   auto* s = new nsw_solver();
+  if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete s;
+    return fail(NSW_ERR_CUDA, "cudaStreamCreate failed");
+  }
   s->dtype = options->dtype;
   s->U = users_local;
   s->n = n;
@@ -386,7 +442,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   nsw_status e = NSW_OK;
 #define ALLOC(p, bytes)                       \
   do {                                        \
-    e = dmalloc(&(p), (bytes));               \
+    e = dmalloc(&(p), (bytes), s->stream);    \
     if (e != NSW_OK) {                        \
       nsw_solver_destroy(s);                  \
       return e;                               \
@@ -430,15 +486,18 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   s->tolbuf = s->own_tol;
   s->U_total = users_local;
 #undef ALLOC
+  // the pool allocations and their zero fills are ordered on the solver's
+  // stream; the synchronous uploads below must not overtake them
+  if (cudaStreamSynchronize(s->stream) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_CUDA, "allocation failed");
+  }
   s->imp_local = s->own_imp_local;
   s->imp_all = world == 1 ? s->own_imp_local : s->own_imp_all;
-  if (cudaMallocHost((void**)&s->state_host, ST_WORDS * sizeof(int)) != cudaSuccess) {
+  static_assert(ST_WORDS * sizeof(int) <= 64, "pinned state block");
+  if ((s->state_host = pinned_state_get()) == nullptr) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaMallocHost failed");
-  }
-  if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
-    nsw_solver_destroy(s);
-    return fail(NSW_ERR_CUDA, "cudaStreamCreate failed");
   }
   if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) != cudaSuccess) {
     nsw_solver_destroy(s);
@@ -540,10 +599,15 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
-                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->flush_buf, s->res, s->iters, s->phase_ns, s->own_tol};
-  for (void* p : bufs)
-    if (p) cudaFree(p);
-  if (s->state_host) cudaFreeHost(s->state_host);
+                  s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->res, s->iters,
+                  s->phase_ns, s->own_tol};
+  if (s->stream) {
+    for (void* p : bufs)
+      if (p) cudaFreeAsync(p, s->stream);   // back to the pool, stream-ordered
+    cudaStreamSynchronize(s->stream);
+  }
+  if (s->flush_buf) cudaFree(s->flush_buf);
+  pinned_state_put(s->state_host);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return NSW_OK;
@@ -720,8 +784,12 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
   if (e != NSW_OK) return e;
   const int steps = s->state_host[ST_STEP];
   if (policy_out) {
-    e = download_converted(s->dtype, s->xbest, policy_out, size_t(s->U) * s->n * s->m);
+    bool nonfinite = false;
+    e = download_converted(s->dtype, s->xbest, policy_out, size_t(s->U) * s->n * s->m, s->stream, &nonfinite);
     if (e != NSW_OK) return e;
+    // the reference's RankingPolicy rejects non-finite entries (core.py:131-148);
+    // the fp32 path checks them on the device while widening
+    if (nonfinite) return fail(NSW_ERR_DOMAIN, "policy contains non-finite entries");
   }
   if (trace) {
     trace->steps = steps;
@@ -782,7 +850,7 @@ nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t
     CUDA_TRY(cudaMemcpy(host, p, c * 8, cudaMemcpyDeviceToHost));
     return NSW_OK;
   }
-  return download_converted(s->dtype, p, host, c);
+  return download_converted(s->dtype, p, host, c, s->stream);
 }
 
 nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, size_t count) {

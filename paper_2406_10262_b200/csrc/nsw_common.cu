@@ -210,6 +210,16 @@ __global__ void flush_kernel(float* buf, size_t n) {
     buf[i] = buf[i] * 0.5f + 1.0f;
 }
 
+__global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, size_t n, unsigned* bad) {
+  bool ok = true;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const float x = src[i];
+    ok &= isfinite(x);
+    dst[i] = double(x);
+  }
+  if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+}
+
 __global__ void discard_kernel(float* buf, size_t n) {
   // one discard per 128-byte line (n floats, 128-byte aligned buffer)
   for (size_t l = blockIdx.x * size_t(blockDim.x) + threadIdx.x; l < n / 32; l += size_t(gridDim.x) * blockDim.x)

@@ -1086,5 +1086,6 @@ __global__ void finalize_kernel(FinalizeArgs f);
 __global__ void stamp_kernel(unsigned long long* stamp);
 __global__ void flush_kernel(float* buf, size_t n);
 __global__ void discard_kernel(float* buf, size_t n);
+__global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, size_t n, unsigned* bad);
 
 }  // namespace nsw

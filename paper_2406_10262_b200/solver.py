@@ -282,7 +282,7 @@ class DeviceSolver:
     def result(self):
         """(best policy float64 [U][n][m], SolveTrace)."""
         J = self.config.outer_max_iters
-        pol = np.empty((self.U, self.n, self.m), dtype=np.float64)
+        pol = _host_buffer((self.U, self.n, self.m))
         obj = np.zeros(J)
         gn = np.zeros(J)
         its = np.zeros(J, dtype=np.int32)
@@ -299,6 +299,19 @@ class DeviceSolver:
             e.trace = trace  # the steps recorded before the failure
             raise
         return pol, trace
+
+
+def _host_buffer(shape) -> np.ndarray:
+    """float64 host array for a device result: page-locked through torch's
+    caching host allocator when torch is present (the copy runs at full link
+    speed and repeated solves reuse the block), else pageable."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:
+        pass
+    return np.empty(shape, dtype=np.float64)
 
 
 def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOptions | None = None):
@@ -319,7 +332,7 @@ def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOption
     J = config.outer_max_iters
     rel_c = np.ascontiguousarray(rel, dtype=np.float64)
     expo_c = np.ascontiguousarray(expo, dtype=np.float64)
-    pol = np.empty((U, n, m), dtype=np.float64)
+    pol = _host_buffer((U, n, m))
     obj = np.zeros(J)
     gn = np.zeros(J)
     its = np.zeros(J, dtype=np.int32)
@@ -332,4 +345,5 @@ def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOption
     k = tr.steps
     trace = SolveTrace([float(x) for x in obj[:k]], [float(x) for x in gn[:k]], [int(x) for x in its[:k]],
                        [float(x) for x in wall[:k]])
-    return RankingPolicy(pol), trace
+    # float32 solves verify finiteness on the device while widening the policy
+    return RankingPolicy._adopt(pol, finite_checked=options.dtype == "float32"), trace
