@@ -278,20 +278,24 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   return NSW_OK;
 }
 
-nsw_status launch_impact_reduce(nsw_solver* s, cudaStream_t st) {
+// Single shard with its own exchange buffers: the finalize runs in the
+// impact reduction's last CTA (one launch and one dependency less per step).
+bool fuse_finalize(const nsw_solver* s) { return s->world == 1 && s->imp_all == s->imp_local; }
+
+nsw_status launch_impact_reduce(nsw_solver* s, cudaStream_t st, bool fuse = false) {
   const dim3 grid((s->n + IMP_ITEMS - 1) / IMP_ITEMS, s->imp_chunks);
   impact_reduce_kernel<<<grid, IMP_THREADS, 0, st>>>(s->partial, s->U, s->n, s->imp_chunks, s->split, s->counter,
                                                      s->imp_local, s->state, s->tol, s->res, s->T,
-                                                     s->cfg.sinkhorn_tol);
+                                                     s->cfg.sinkhorn_tol, fuse ? 1 : 0, s->fin);
   CUDA_TRY(cudaGetLastError());
   s->launches += 1;
   return NSW_OK;
 }
 
-nsw_status launch_step(nsw_solver* s, cudaStream_t st) {
+nsw_status launch_step(nsw_solver* s, cudaStream_t st, bool fuse = false) {
   nsw_status e = launch_fused(s, st);
   if (e != NSW_OK) return e;
-  return launch_impact_reduce(s, st);
+  return launch_impact_reduce(s, st, fuse);
 }
 
 nsw_status launch_finalize(nsw_solver* s, cudaStream_t st) {
@@ -671,8 +675,9 @@ static nsw_status ensure_graph(nsw_solver* s) {
   cudaGraph_t g;
   CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
   const int64_t before = s->launches;
-  nsw_status e = launch_step(s, s->stream);
-  if (e == NSW_OK) e = launch_finalize(s, s->stream);
+  const bool fuse = fuse_finalize(s);
+  nsw_status e = launch_step(s, s->stream, fuse);
+  if (e == NSW_OK && !fuse) e = launch_finalize(s, s->stream);
   s->launches = before;
   cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
   if (e != NSW_OK) return e;
@@ -720,8 +725,9 @@ static nsw_status one_step_tolerance(nsw_solver* s) {
       continue;
     }
     if (ph == PHASE_FWD_FIN) {
-      e = launch_step(s, s->stream);  // finish launch + impact reduction
-      if (e != NSW_OK) return e;
+      const bool fuse = fuse_finalize(s);
+      e = launch_step(s, s->stream, fuse);  // finish launch + impact reduction (+ finalize)
+      if (e != NSW_OK || fuse) return e;
     }
     return launch_finalize(s, s->stream);
   }
@@ -733,11 +739,12 @@ static nsw_status one_step(nsw_solver* s) {
     nsw_status e = ensure_graph(s);
     if (e != NSW_OK) return e;
     CUDA_TRY(cudaGraphLaunch(s->gexec, s->stream));
-    s->launches += 3;
+    s->launches += (s->U1 > 0 && s->U1 < s->U ? 2 : 1) + (fuse_finalize(s) ? 1 : 2);
     return NSW_OK;
   }
-  nsw_status e = launch_step(s, s->stream);
-  if (e != NSW_OK) return e;
+  const bool fuse = fuse_finalize(s);
+  nsw_status e = launch_step(s, s->stream, fuse);
+  if (e != NSW_OK || fuse) return e;
   return launch_finalize(s, s->stream);
 }
 
@@ -934,12 +941,15 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
     nsw_status e = launch_fused(s, s->stream);
     if (e != NSW_OK) return e;
     CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
-    e = launch_impact_reduce(s, s->stream);
+    const bool fuse = fuse_finalize(s);
+    e = launch_impact_reduce(s, s->stream, fuse);
     if (e != NSW_OK) return e;
-    finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
-    CUDA_TRY(cudaGetLastError());
+    if (!fuse) {
+      finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
+      CUDA_TRY(cudaGetLastError());
+      s->launches += 1;
+    }
     CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));
-    s->launches += 2;
   }
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   float tot = 0.f, fus = 0.f;

@@ -14,6 +14,9 @@ __device__ __forceinline__ bool forward_ready(int phase, int tol_mode) {
                   : (phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME);
 }
 
+template <int NTH>
+__device__ void finalize_body(const FinalizeArgs& f, double* sF, double* sG, int& sBad, int& sConv);
+
 // Two-level, fixed-order reduction.  Level 1: CTA (x, y) sums items
 // [8x, 8x+8) over user chunk y (thread t: item t % IMP_ITEMS, user lane
 // t / IMP_ITEMS, then a fixed shared-memory tree) into split[y][i].  Level
@@ -24,8 +27,15 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
                                                                     double* __restrict__ imp_local,
                                                                     const int* __restrict__ state, int tol_mode,
                                                                     const double* __restrict__ res, int T,
-                                                                    double tol) {
-  if (!forward_ready(state[ST_PHASE], tol_mode)) return;
+                                                                    double tol, int fuse_finalize, FinalizeArgs fin) {
+  const int phase0 = state[ST_PHASE];
+  if (!forward_ready(phase0, tol_mode)) {
+    // single shard: the step's finalize is fused here, including the
+    // DONE_PENDING -> FINISHED transition of a launch with no forward
+    if (fuse_finalize && phase0 == PHASE_DONE_PENDING && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
+      fin.state[ST_PHASE] = PHASE_FINISHED;
+    return;
+  }
   constexpr int LANES = IMP_THREADS / IMP_ITEMS;
   __shared__ double red[IMP_THREADS];
   __shared__ bool last;
@@ -78,6 +88,14 @@ __global__ void __launch_bounds__(IMP_THREADS) impact_reduce_kernel(const double
     imp_local[n] = double(sc);
     *counter = 0u;
   }
+  if (fuse_finalize) {
+    __shared__ double sF[512];
+    __shared__ double sG[512];
+    __shared__ int sBad, sConv;
+    __threadfence_block();
+    __syncthreads();
+    finalize_body<IMP_THREADS>(fin, sF, sG, sBad, sConv);
+  }
 }
 
 __global__ void __launch_bounds__(256) tol_chunk_max_kernel(const double* __restrict__ res, int U, int T,
@@ -124,19 +142,16 @@ __global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int ch
   }
 }
 
-__global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
+// Objective, gradient norm, trace, best iterate, stop and error decisions
+// from the (gathered) impacts.  The sums run over 512 virtual lanes in a fixed
+// tree whatever the block size (NTH threads take 512 / NTH lanes each), so
+// the standalone kernel and the copy fused into the impact reduction give
+// bitwise-identical results.
+template <int NTH>
+__device__ void finalize_body(const FinalizeArgs& f, double* sF, double* sG, int& sBad, int& sConv) {
   constexpr int NT = 512;
-  __shared__ double sF[NT];
-  __shared__ double sG[NT];
-  __shared__ int sBad, sConv;
+  static_assert(NT % NTH == 0, "virtual lanes");
   const int tid = threadIdx.x;
-  const int phase = f.state[ST_PHASE];
-  if (phase == PHASE_FINISHED) return;
-  if (phase == PHASE_DONE_PENDING) {
-    if (tid == 0) f.state[ST_PHASE] = PHASE_FINISHED;
-    return;
-  }
-  if (!forward_ready(phase, f.tol_mode)) return;
   if (tid == 0) {
     sBad = 0;
     sConv = 0;
@@ -150,24 +165,26 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
     for (int g = 0; g < f.world; ++g) c += f.imp_all[size_t(g) * (f.n + 1) + f.n];
     sConv = int(c);
   }
-  double accF = 0.0, accG = 0.0;
   int bad = 0;
-  for (int i = tid; i < f.n; i += NT) {
-    double imp = 0.0;
-    for (int g = 0; g < f.world; ++g) imp += f.imp_all[size_t(g) * (f.n + 1) + i];
-    f.imp_cur[i] = imp;
-    if (!(imp > 0.0) || !isfinite(imp)) bad = 1;
-    accF += log(imp);
-    accG += f.rel_sq[i] * f.exp_sq / (imp * imp);
+  for (int v = tid; v < NT; v += NTH) {
+    double accF = 0.0, accG = 0.0;
+    for (int i = v; i < f.n; i += NT) {
+      double imp = 0.0;
+      for (int g = 0; g < f.world; ++g) imp += f.imp_all[size_t(g) * (f.n + 1) + i];
+      f.imp_cur[i] = imp;
+      if (!(imp > 0.0) || !isfinite(imp)) bad = 1;
+      accF += log(imp);
+      accG += f.rel_sq[i] * f.exp_sq / (imp * imp);
+    }
+    sF[v] = accF;
+    sG[v] = accG;
   }
   if (bad) atomicOr(&sBad, 1);
-  sF[tid] = accF;
-  sG[tid] = accG;
   __syncthreads();
   for (int w = NT / 2; w > 0; w >>= 1) {
-    if (tid < w) {
-      sF[tid] += sF[tid + w];
-      sG[tid] += sG[tid + w];
+    for (int v = tid; v < w; v += NTH) {
+      sF[v] += sF[v + w];
+      sG[v] += sG[v + w];
     }
     __syncthreads();
   }
@@ -201,6 +218,21 @@ __global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
   f.state[ST_STEP] = k1;
   f.state[ST_IMPROVED] = improved;
   f.state[ST_PHASE] = (gn <= f.grad_threshold || k1 >= f.outer_max) ? PHASE_DONE_PENDING : PHASE_RUNNING;
+}
+
+
+__global__ void __launch_bounds__(512) finalize_kernel(FinalizeArgs f) {
+  __shared__ double sF[512];
+  __shared__ double sG[512];
+  __shared__ int sBad, sConv;
+  const int phase = f.state[ST_PHASE];
+  if (phase == PHASE_FINISHED) return;
+  if (phase == PHASE_DONE_PENDING) {
+    if (threadIdx.x == 0) f.state[ST_PHASE] = PHASE_FINISHED;
+    return;
+  }
+  if (!forward_ready(phase, f.tol_mode)) return;
+  finalize_body<512>(f, sF, sG, sBad, sConv);
 }
 
 __global__ void stamp_kernel(unsigned long long* stamp) { stamp[0] = globaltimer_ns(); }

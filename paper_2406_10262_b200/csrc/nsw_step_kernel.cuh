@@ -1044,25 +1044,6 @@ forward_iterations:
 // --------------------------------------------------------------------------
 constexpr int IMP_THREADS = 256;
 constexpr int IMP_ITEMS = 8;
-// imp_local has n + 1 slots: the n impacts and, in tolerance mode, this
-// shard's count of users whose residual at t* is <= tol (the exchange
-// carries it to every rank for the SolverError guard).
-__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n, int chunks,
-                                     double* __restrict__ split, unsigned int* counter,
-                                     double* __restrict__ imp_local, const int* __restrict__ state, int tol_mode,
-                                     const double* __restrict__ res, int T, double tol);
-
-// Tolerance mode, after each forward chunk, the lock-step stopping test of
-// sinkhorn.py:244 in two parts so the ranks of a sharded solve can combine
-// their maxima in between (all-reduce MAX, in place):
-//   tol_chunk_max_kernel: cmax[j] = max over this shard's users of the
-//     residual after iteration t0+1+j of the chunk;
-//   tol_decide_kernel: t* = first iteration whose (global) max is <= tol;
-//     sets PHASE_FWD_FIN (t* found or the budget is spent) or PHASE_FWD_CONT.
-__global__ void tol_chunk_max_kernel(const double* __restrict__ res, int U, int T, int chunk, const int* state,
-                                     double* __restrict__ cmax);
-__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state);
-
 struct FinalizeArgs {
   int n, world, outer_max;
   const double* imp_all;   // [world][n + 1]: impacts + converged-user count per rank
@@ -1081,6 +1062,27 @@ struct FinalizeArgs {
   const double* res;       // [U][T+1] residuals (tolerance mode)
   int* iters;              // [outer_max] inner iterations per step (trace)
 };
+
+// imp_local has n + 1 slots: the n impacts and, in tolerance mode, this
+// shard's count of users whose residual at t* is <= tol (the exchange
+// carries it to every rank for the SolverError guard).
+__global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, int n, int chunks,
+                                     double* __restrict__ split, unsigned int* counter,
+                                     double* __restrict__ imp_local, const int* __restrict__ state, int tol_mode,
+                                     const double* __restrict__ res, int T, double tol, int fuse_finalize,
+                                     FinalizeArgs fin);
+
+// Tolerance mode, after each forward chunk, the lock-step stopping test of
+// sinkhorn.py:244 in two parts so the ranks of a sharded solve can combine
+// their maxima in between (all-reduce MAX, in place):
+//   tol_chunk_max_kernel: cmax[j] = max over this shard's users of the
+//     residual after iteration t0+1+j of the chunk;
+//   tol_decide_kernel: t* = first iteration whose (global) max is <= tol;
+//     sets PHASE_FWD_FIN (t* found or the budget is spent) or PHASE_FWD_CONT.
+__global__ void tol_chunk_max_kernel(const double* __restrict__ res, int U, int T, int chunk, const int* state,
+                                     double* __restrict__ cmax);
+__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state);
+
 
 __global__ void finalize_kernel(FinalizeArgs f);
 __global__ void stamp_kernel(unsigned long long* stamp);
