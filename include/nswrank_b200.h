@@ -150,6 +150,10 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
  * ([U][m-1] int32).  The reference has no ranking extraction; this is the
  * definition of SURVEY.md 8(a) (numpy argmax over items). */
 nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host);
+/* Evaluation metrics (reference metrics.py) of the best policy, on the
+ * device where it lives: out_host[4] as nsw_policy_metrics_*.  This
+ * shard's users only (a sharded solve evaluates its block). */
+nsw_status nsw_solver_metrics(nsw_solver* s, double threshold, double* out_host);
 
 /* Raw state access for tests and one-step parity (host float64 buffers):
  * field = "cost" | "adam_m" | "adam_v" [U][n][m], "alpha" [U][n], "beta" [U][m],
@@ -177,6 +181,16 @@ nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count);
  * into device int32 out [U][m-1], on `stream` (cudaStream_t, 0 = default). */
 nsw_status nsw_top_positions_f32(const float* X, int32_t U, int32_t n, int32_t m, int32_t* out, void* stream);
 nsw_status nsw_top_positions_f64(const double* X, int32_t U, int32_t n, int32_t m, int32_t* out, void* stream);
+
+/* Policy evaluation metrics (reference metrics.py:16-69) of a device policy
+ * X [U][n][m] with device relevance [U][n] (same scalar type) and host
+ * exposures [m-1] float64: out_host[0..3] = user_utility, mean_max_envy,
+ * items_better_off(threshold), items_worse_off(threshold).  float64
+ * accumulation; the n x n x U envy product is a cuBLAS DGEMM. */
+nsw_status nsw_policy_metrics_f32(const float* X, const float* rel, const double* expo, int32_t U, int32_t n,
+                                  int32_t m, double threshold, double* out_host, void* stream);
+nsw_status nsw_policy_metrics_f64(const double* X, const double* rel, const double* expo, int32_t U, int32_t n,
+                                  int32_t m, double threshold, double* out_host, void* stream);
 
 /* ------------------------------------------------------------------------ *
  * 3. Inner operator seam (device pointers, fixed schedule).                *

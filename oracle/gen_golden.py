@@ -198,10 +198,37 @@ def case_tolerance_desk():
              sinkhorn_iterations=np.array(tr.sinkhorn_iterations))
 
 
+def case_metrics():
+    """The reference's metrics (metrics.py) on the cfg0 golden policy and on
+    a cfg1-slice policy; pins oracle.policy_metrics against them."""
+    import nswrank.metrics as ref_metrics
+    out = {}
+    g = np.load(os.path.join(OUT, "cfg0_fixed.npz"))
+    rel, expo, pol = g["relevance"], g["exposure"], g["policy"]
+    rel2, expo2, _ = make_instance("cfg1", seed=0, user_slice=(0, 16))
+    rng = np.random.default_rng(3)
+    pol2 = rng.random((16, rel2.shape[1], expo2.size + 1))
+    pol2 /= pol2.sum(axis=1, keepdims=True)       # any nonnegative tensor is a valid metric input
+    for tag, (r, e, x) in {"cfg0": (rel, expo, pol), "cfg1s": (rel2, expo2, pol2)}.items():
+        U, n = r.shape
+        R, E, P = nswrank.RelevanceMatrix(r), nswrank.ExposureModel(e), nswrank.RankingPolicy(x)
+        ref = np.array([ref_metrics.user_utility(P, R, E), ref_metrics.mean_max_envy(P, R, E),
+                        ref_metrics.items_better_off(P, R, E), ref_metrics.items_worse_off(P, R, E),
+                        ref_metrics.items_better_off(P, R, E, threshold=0.02),
+                        ref_metrics.items_worse_off(P, R, E, threshold=0.02)])
+        mine = np.array(orc.policy_metrics(x, r, e) + orc.policy_metrics(x, r, e, 0.02)[2:])
+        assert np.array_equal(ref, mine), (tag, ref, mine)
+        out[f"{tag}_relevance"], out[f"{tag}_exposure"], out[f"{tag}_policy"] = r, e, x
+        out[f"{tag}_metrics"] = ref
+        print(f"metrics {tag}: {ref}")
+    np.savez(os.path.join(OUT, "metrics.npz"), **out)
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["ops", "cfg0", "tol", "cfg1"]
+    which = sys.argv[1:] or ["ops", "cfg0", "tol", "cfg1", "metrics"]
     for w in which:
         t = time.time()
-        {"ops": case_ops, "cfg0": case_cfg0, "tol": case_tolerance_desk, "cfg1": case_cfg1_slice}[w]()
+        {"ops": case_ops, "cfg0": case_cfg0, "tol": case_tolerance_desk, "cfg1": case_cfg1_slice,
+         "metrics": case_metrics}[w]()
         print(f"  {w}: {time.time() - t:.1f}s")

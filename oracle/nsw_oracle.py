@@ -315,6 +315,29 @@ def one_step(rel, expo, state, p: SolverParams, dtype=np.float64):
                 log_v=fwd.log_v, log_u=fwd.log_u)
 
 
+# --------------------------------------------------------------------------
+# evaluation metrics  (metrics.py:16-69)
+# --------------------------------------------------------------------------
+def policy_metrics(policy, rel, expo, threshold=0.10):
+    """user_utility, mean_max_envy, items_better_off, items_worse_off of a
+    policy (metrics.py:16-22, :25-41, :44-52, :55-63; uniform reference
+    policy core.py:220-231)."""
+    U, n, m = policy.shape
+    x = policy[:, :, : m - 1]
+    util = float(np.einsum("ui,k,uik->", rel, expo, x) / U)               # metrics.py:20-22
+    alloc = np.einsum("ujk,k->uj", x, expo)                               # metrics.py:37
+    cross = rel.T @ alloc                                                  # metrics.py:39
+    envy = float((cross.max(axis=1) - np.diagonal(cross)).mean())         # metrics.py:40-41
+    imp = impact(rel, expo, policy)
+    unif = np.empty((U, n, m))
+    unif[:, :, : m - 1] = 1.0 / n
+    unif[:, :, m - 1] = (n - m + 1) / n
+    imp_u = impact(rel, expo, unif)                                        # metrics.py:66-68
+    better = float(np.mean(imp > (1.0 + threshold) * imp_u))
+    worse = float(np.mean(imp < (1.0 - threshold) * imp_u))
+    return util, envy, better, worse
+
+
 def top_positions(policy):
     """Top-m ranking used for the bit-exact ranking check: for every user and
     real position k, argmax_i X[u, i, k] (numpy first-index tie-break).

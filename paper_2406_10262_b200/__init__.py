@@ -15,6 +15,7 @@ _EXPORTS = {
     "data": ("exposure_model", "make_instance", "BASELINE_CONFIGS"),
     "sinkhorn": ("sinkhorn_batch", "sinkhorn_backward_batch"),
     "ranking": ("top_positions",),
+    "metrics": ("user_utility", "mean_max_envy", "items_better_off", "items_worse_off", "policy_metrics"),
     "distributed": ("solve_fair_ranking_distributed", "shard_users"),
 }
 

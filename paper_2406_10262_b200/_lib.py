@@ -71,11 +71,14 @@ SIGNATURES = {
     "nsw_solver_time_steps":(C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "nsw_solver_phase_times": (C.c_int, [_vp, C.POINTER(C.c_uint64), _i32]),
     "nsw_solver_top_positions": (C.c_int, [_vp, C.POINTER(_i32)]),
+    "nsw_solver_metrics": (C.c_int, [_vp, C.c_double, _dp]),
     "nsw_solver_bind_tol_exchange": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_local": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_decide": (C.c_int, [_vp, _vp, C.POINTER(_i32)]),
     "nsw_top_positions_f32": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "nsw_top_positions_f64": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "nsw_policy_metrics_f32": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
+    "nsw_policy_metrics_f64": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
     "nsw_sinkhorn_batch_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_batch_f32": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_backward_batch_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),

@@ -54,7 +54,7 @@ def _jobs():
     for f64 in (0, 1):
         jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(BUILD, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
                      [f"-DNSW_F64={f64}"]))
-    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank"):
+    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics"):
         jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(BUILD, name + ".o"), []))
     return jobs
 
@@ -86,7 +86,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         tmp = LIB + ".tmp"
-        cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs]
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcublas"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr}")

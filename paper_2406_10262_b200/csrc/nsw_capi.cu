@@ -136,6 +136,7 @@ struct nsw_solver {
   double* own_tol = nullptr;         // [chunk] per-iteration residual maxima (tolerance mode)
   double* tolbuf = nullptr;          // bound exchange buffer for them (all-reduce MAX in place)
   int U_total = 0;                   // users over all ranks
+  std::vector<double> expo_host;     // exposures [m-1] (metrics)
   cudaStream_t stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
   bool graph_dirty = true;
@@ -551,6 +552,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return e;
   }
+  s->expo_host.assign(exposure, exposure + (m - 1));
   std::vector<double> ex(m, 0.0);
   double exp_sq = 0.0;
   for (int k = 0; k < m - 1; ++k) {
@@ -982,6 +984,20 @@ nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host) {
   }
   cudaFree(d);
   return e;
+}
+
+nsw_status nsw_solver_metrics(nsw_solver* s, double threshold, double* out_host) {
+  if (!s || !out_host) return fail(NSW_ERR_ARG, "NULL argument");
+  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  const nsw_status e =
+      s->dtype == NSW_F64
+          ? nsw_policy_metrics_f64((const double*)s->xbest, (const double*)s->rel, s->expo_host.data(), s->U, s->n,
+                                   s->m, threshold, out_host, s->stream)
+          : nsw_policy_metrics_f32((const float*)s->xbest, (const float*)s->rel, s->expo_host.data(), s->U, s->n,
+                                   s->m, threshold, out_host, s->stream);
+  if (e != NSW_OK) return fail(e, "policy metrics failed");
+  s->launches += 5;
+  return NSW_OK;
 }
 
 nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count) {

@@ -1,0 +1,175 @@
+// Policy evaluation metrics on the device (reference metrics.py:16-69):
+//   user_utility     = sum_{u,i,k<m-1} r_ui e_k x_uik / |U|
+//   mean_max_envy    = mean_i ( max_j cross_ij - cross_ii ),
+//                      cross = R^T A, A_uj = sum_{k<m-1} x_ujk e_k
+//   items_better_off = mean_i [ Imp_i > (1 + th) Imp^unif_i ]
+//   items_worse_off  = mean_i [ Imp_i < (1 - th) Imp^unif_i ]
+// Everything is accumulated in float64 in a fixed order (deterministic).
+// The one dense product (cross, n x n x |U|) is a plain cuBLAS DGEMM; the
+// allocation masses, impacts and row maxima are kernels here.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "../../include/nswrank_b200.h"
+
+namespace nsw {
+namespace {
+
+__global__ void widen_to_f64(const float* __restrict__ src, double* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = double(src[i]);
+}
+
+// A_uj = sum_{k<m-1} x_ujk e_k  (float64), one thread per (u, j)
+template <typename S>
+__global__ void alloc_kernel(const S* __restrict__ X, const double* __restrict__ e, int U, int n, int m,
+                             double* __restrict__ A) {
+  const size_t cells = size_t(U) * n;
+  for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < cells; q += size_t(gridDim.x) * blockDim.x) {
+    const S* x = X + q * m;
+    double acc = 0.0;
+    for (int k = 0; k < m - 1; ++k) acc += double(x[k]) * e[k];
+    A[q] = acc;
+  }
+}
+
+// Imp_j = sum_u r_uj A_uj and Imp^unif_j = (sum_k e_k / n) sum_u r_uj, users
+// in index order; one thread per item (coalesced over items)
+template <typename S>
+__global__ void impact_kernel(const S* __restrict__ rel, const double* __restrict__ A, int U, int n,
+                              double e_sum_over_n, double* __restrict__ imp, double* __restrict__ imp_unif) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double a = 0.0, b = 0.0;
+  for (int u = 0; u < U; ++u) {
+    const double r = double(rel[size_t(u) * n + j]);
+    a += r * A[size_t(u) * n + j];
+    b += r;
+  }
+  imp[j] = a;
+  imp_unif[j] = b * e_sum_over_n;
+}
+
+// envy_i = max_j cross(i, j) - cross(i, i); cross column-major (n x n)
+__global__ void envy_kernel(const double* __restrict__ cross, int n, double* __restrict__ envy) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double mx = -INFINITY;
+  for (int j = 0; j < n; ++j) mx = fmax(mx, cross[size_t(j) * n + i]);
+  envy[i] = mx - cross[size_t(i) * n + i];
+}
+
+// one block: the four metrics from the per-item vectors, fixed-order sums
+__global__ void metrics_finish_kernel(const double* __restrict__ imp, const double* __restrict__ imp_unif,
+                                      const double* __restrict__ envy, int n, int U, double th,
+                                      double* __restrict__ out) {
+  __shared__ double s_imp[256], s_env[256];
+  __shared__ int s_b[256], s_w[256];
+  double a = 0.0, c = 0.0;
+  int b = 0, w = 0;
+  for (int i = threadIdx.x; i < n; i += 256) {
+    a += imp[i];
+    c += envy[i];
+    b += imp[i] > (1.0 + th) * imp_unif[i];
+    w += imp[i] < (1.0 - th) * imp_unif[i];
+  }
+  s_imp[threadIdx.x] = a;
+  s_env[threadIdx.x] = c;
+  s_b[threadIdx.x] = b;
+  s_w[threadIdx.x] = w;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      s_imp[threadIdx.x] += s_imp[threadIdx.x + s];
+      s_env[threadIdx.x] += s_env[threadIdx.x + s];
+      s_b[threadIdx.x] += s_b[threadIdx.x + s];
+      s_w[threadIdx.x] += s_w[threadIdx.x + s];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = s_imp[0] / double(U);
+    out[1] = s_env[0] / double(n);
+    out[2] = double(s_b[0]) / double(n);
+    out[3] = double(s_w[0]) / double(n);
+  }
+}
+
+template <typename S>
+nsw_status policy_metrics(const void* X, const void* rel, const double* expo_host, int32_t U, int32_t n,
+                          int32_t m, double threshold, double* out_host, void* stream) {
+  if (!X || !rel || !expo_host || !out_host) return NSW_ERR_ARG;
+  if (U <= 0 || n <= 0 || m < 2 || m > n) return NSW_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t cells = size_t(U) * n;
+  double* buf = nullptr;   // e[m] | A[U n] | cross[n n] | imp[n] | unif[n] | envy[n] | out[4]
+  const size_t words = size_t(m) + cells + size_t(n) * n + 3 * size_t(n) + 4;
+  if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  double* e = buf;
+  double* A = e + m;
+  double* cross = A + cells;
+  double* imp = cross + size_t(n) * n;
+  double* unif = imp + n;
+  double* envy = unif + n;
+  double* out = envy + n;
+  double esum = 0.0;
+  for (int k = 0; k < m - 1; ++k) esum += expo_host[k];
+  nsw_status status = NSW_OK;
+  cublasHandle_t h = nullptr;
+  const double one = 1.0, zero = 0.0;
+  if (cudaMemcpyAsync(e, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    status = NSW_ERR_CUDA;
+  } else {
+    alloc_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
+    impact_kernel<S><<<(n + 127) / 128, 128, 0, st>>>(static_cast<const S*>(rel), A, U, n, esum / n, imp, unif);
+    // cross(i, j) = sum_u r_ui A_uj: column-major n x n = R' A with R, A
+    // read as column-major n x U matrices (their row-major [U][n] layout)
+    double* Rd = nullptr;
+    if constexpr (sizeof(S) == 8) {
+      Rd = const_cast<double*>(static_cast<const double*>(rel));
+    } else {
+      // widen R for DGEMM (float64 products, as the reference's numpy matmul)
+      if (cudaMallocAsync((void**)&Rd, cells * sizeof(double), st) != cudaSuccess) status = NSW_ERR_CUDA;
+      else widen_to_f64<<<148 * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
+    }
+    if (status == NSW_OK && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
+    if (status == NSW_OK && cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
+    if (status == NSW_OK &&
+        cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, U, &one, Rd, n, A, n, &zero, cross, n) != CUBLAS_STATUS_SUCCESS)
+      status = NSW_ERR_CUDA;
+    if (status == NSW_OK) {
+      envy_kernel<<<(n + 127) / 128, 128, 0, st>>>(cross, n, envy);
+      metrics_finish_kernel<<<1, 256, 0, st>>>(imp, unif, envy, n, U, threshold, out);
+      if (cudaGetLastError() != cudaSuccess ||
+          cudaMemcpyAsync(out_host, out, 4 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        status = NSW_ERR_CUDA;
+    }
+    if constexpr (sizeof(S) == 4) {
+      if (Rd) cudaFreeAsync(Rd, st);
+    }
+  }
+  cudaFreeAsync(buf, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) status = NSW_ERR_CUDA;
+  if (h) cublasDestroy(h);
+  return status;
+}
+
+}  // namespace
+}  // namespace nsw
+
+extern "C" {
+
+nsw_status nsw_policy_metrics_f32(const float* X, const float* rel, const double* expo, int32_t U, int32_t n,
+                                  int32_t m, double threshold, double* out, void* stream) {
+  return nsw::policy_metrics<float>(X, rel, expo, U, n, m, threshold, out, stream);
+}
+
+nsw_status nsw_policy_metrics_f64(const double* X, const double* rel, const double* expo, int32_t U, int32_t n,
+                                  int32_t m, double threshold, double* out, void* stream) {
+  return nsw::policy_metrics<double>(X, rel, expo, U, n, m, threshold, out, stream);
+}
+
+}  // extern "C"

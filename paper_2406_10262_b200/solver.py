@@ -279,6 +279,13 @@ class DeviceSolver:
         check(self.lib.nsw_solver_top_positions(self.h, out.ctypes.data_as(C.POINTER(C.c_int32))), "top_positions")
         return out
 
+    def metrics(self, threshold: float = 0.10) -> dict:
+        """Reference metrics (metrics.py) of the best policy, computed where it lives."""
+        out = np.zeros(4)
+        check(self.lib.nsw_solver_metrics(self.h, float(threshold), _lib.dptr(out)), "metrics")
+        return {"user_utility": float(out[0]), "mean_max_envy": float(out[1]),
+                "items_better_off": float(out[2]), "items_worse_off": float(out[3])}
+
     def result(self):
         """(best policy float64 [U][n][m], SolveTrace)."""
         J = self.config.outer_max_iters

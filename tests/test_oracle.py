@@ -145,3 +145,13 @@ def test_generator_user_slice_matches_full():
     full, _, _ = make_instance("cfg1", seed=3, num_users=40)
     part, _, _ = make_instance("cfg1", seed=3, num_users=40, user_slice=(10, 25))
     assert np.array_equal(full[10:25], part)
+
+
+def test_metrics_restatement_matches_reference_values(golden):
+    """oracle.policy_metrics reproduces nswrank.metrics bit-for-bit (values
+    generated from the reference by oracle/gen_golden.py)."""
+    g = golden("metrics")
+    for tag in ("cfg0", "cfg1s"):
+        r, e, x, ref = g[f"{tag}_relevance"], g[f"{tag}_exposure"], g[f"{tag}_policy"], g[f"{tag}_metrics"]
+        got = np.array(orc.policy_metrics(x, r, e) + orc.policy_metrics(x, r, e, 0.02)[2:])
+        assert np.array_equal(got, ref)
