@@ -10,6 +10,7 @@
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 
@@ -36,18 +37,35 @@ __global__ void alloc_kernel(const S* __restrict__ X, const double* __restrict__
   }
 }
 
-// Imp_j = sum_u r_uj A_uj and Imp^unif_j = (sum_k e_k / n) sum_u r_uj, users
-// in index order; one thread per item (coalesced over items)
+// Imp_j = sum_u r_uj A_uj and Imp^unif_j = (sum_k e_k / n) sum_u r_uj in two
+// fixed-order levels: chunk c of the users (grid.y) sums its users in index
+// order per item (coalesced over items), then chunk partials add in chunk order
 template <typename S>
-__global__ void impact_kernel(const S* __restrict__ rel, const double* __restrict__ A, int U, int n,
-                              double e_sum_over_n, double* __restrict__ imp, double* __restrict__ imp_unif) {
+__global__ void impact_partial_kernel(const S* __restrict__ rel, const double* __restrict__ A, int U, int n,
+                                      int chunks, double* __restrict__ pa, double* __restrict__ pb) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
+  const int c = blockIdx.y;
+  const int ub = int((long long)c * U / chunks), ue = int((long long)(c + 1) * U / chunks);
   double a = 0.0, b = 0.0;
-  for (int u = 0; u < U; ++u) {
+  for (int u = ub; u < ue; ++u) {
     const double r = double(rel[size_t(u) * n + j]);
     a += r * A[size_t(u) * n + j];
     b += r;
+  }
+  pa[size_t(c) * n + j] = a;
+  pb[size_t(c) * n + j] = b;
+}
+
+__global__ void impact_combine_kernel(const double* __restrict__ pa, const double* __restrict__ pb, int n,
+                                      int chunks, double e_sum_over_n, double* __restrict__ imp,
+                                      double* __restrict__ imp_unif) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double a = 0.0, b = 0.0;
+  for (int c = 0; c < chunks; ++c) {
+    a += pa[size_t(c) * n + j];
+    b += pb[size_t(c) * n + j];
   }
   imp[j] = a;
   imp_unif[j] = b * e_sum_over_n;
@@ -98,6 +116,15 @@ __global__ void metrics_finish_kernel(const double* __restrict__ imp, const doub
   }
 }
 
+// one cuBLAS handle per host thread and device (creating one costs ms)
+cublasHandle_t cublas_handle() {
+  thread_local cublasHandle_t handles[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
+  return handles[dev];
+}
+
 template <typename S>
 nsw_status policy_metrics(const void* X, const void* rel, const double* expo_host, int32_t U, int32_t n,
                           int32_t m, double threshold, double* out_host, void* stream) {
@@ -105,8 +132,18 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   if (U <= 0 || n <= 0 || m < 2 || m > n) return NSW_ERR_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t cells = size_t(U) * n;
-  double* buf = nullptr;   // e[m] | A[U n] | cross[n n] | imp[n] | unif[n] | envy[n] | out[4]
-  const size_t words = size_t(m) + cells + size_t(n) * n + 3 * size_t(n) + 4;
+  // user chunks of the impact sums: ~4 CTAs of 128 items per SM
+  const int chunks = std::max(1, std::min(U, (148 * 4 * 128 + n - 1) / n));
+  double* buf = nullptr;   // e[m] | A[U n] | cross[n n] | imp[n] | unif[n] | envy[n] | out[4] | pa, pb [chunks n]
+  const size_t words = size_t(m) + cells + size_t(n) * n + 3 * size_t(n) + 4 + 2 * size_t(chunks) * n;
+  {
+    // keep the pool's memory between calls (large transient buffers)
+    int dev = 0;
+    cudaMemPool_t pool;
+    uint64_t keep = ~uint64_t(0);
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
   if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
   double* e = buf;
   double* A = e + m;
@@ -115,6 +152,8 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   double* unif = imp + n;
   double* envy = unif + n;
   double* out = envy + n;
+  double* pa = out + 4;
+  double* pb = pa + size_t(chunks) * n;
   double esum = 0.0;
   for (int k = 0; k < m - 1; ++k) esum += expo_host[k];
   nsw_status status = NSW_OK;
@@ -124,7 +163,9 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
     status = NSW_ERR_CUDA;
   } else {
     alloc_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
-    impact_kernel<S><<<(n + 127) / 128, 128, 0, st>>>(static_cast<const S*>(rel), A, U, n, esum / n, imp, unif);
+    impact_partial_kernel<S><<<dim3((n + 127) / 128, chunks), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n,
+                                                                             chunks, pa, pb);
+    impact_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(pa, pb, n, chunks, esum / n, imp, unif);
     // cross(i, j) = sum_u r_ui A_uj: column-major n x n = R' A with R, A
     // read as column-major n x U matrices (their row-major [U][n] layout)
     double* Rd = nullptr;
@@ -135,7 +176,7 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
       if (cudaMallocAsync((void**)&Rd, cells * sizeof(double), st) != cudaSuccess) status = NSW_ERR_CUDA;
       else widen_to_f64<<<148 * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
     }
-    if (status == NSW_OK && cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
+    if (status == NSW_OK && (h = cublas_handle()) == nullptr) status = NSW_ERR_CUDA;
     if (status == NSW_OK && cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
     if (status == NSW_OK &&
         cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, U, &one, Rd, n, A, n, &zero, cross, n) != CUBLAS_STATUS_SUCCESS)
@@ -153,7 +194,6 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   }
   cudaFreeAsync(buf, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) status = NSW_ERR_CUDA;
-  if (h) cublasDestroy(h);
   return status;
 }
 
