@@ -193,15 +193,34 @@ nsw_status nsw_policy_metrics_f64(const double* X, const double* rel, const doub
                                   int32_t m, double threshold, double* out_host, void* stream);
 
 /* ------------------------------------------------------------------------ *
- * 3. Inner operator seam (device pointers, fixed schedule).                *
- *    nsw_sinkhorn_batch_*  replaces _sinkhorn_batch(..., tol<=0, record)   *
- *        (reference sinkhorn.py:204-255): log_kernel [B][n][m],            *
- *        log_v_init [B][m] -> plan [B][n][m], log_u [B][n], log_v [B][m],  *
- *        log_v_hist [T][B][m].                                             *
- *    nsw_sinkhorn_backward_batch_* replaces _sinkhorn_backward_batch       *
- *        (reference sinkhorn.py:258-309) -> grad_log_kernel [B][n][m].     *
- *    Marginals are the ranking marginals (sinkhorn.py:55-60).              *
+ * 3. Inner operator seam (device pointers; one CTA per batch element).     *
+ *    nsw_sinkhorn_solve_batch_* replaces _sinkhorn_batch (reference         *
+ *        sinkhorn.py:204-255) with its full contract: log_kernel [B][n][m], *
+ *        row [n] and col [m] masses (NULL, NULL = the ranking marginals of  *
+ *        sinkhorn.py:55-60), log_v_init [B][m], tol (<= 0: exactly         *
+ *        max_iters iterations; > 0: lock-step stop over the batch when the  *
+ *        largest L-inf marginal residual is <= tol, sinkhorn.py:237-246)   *
+ *        -> plan [B][n][m], log_u [B][n], log_v [B][m], log_v_hist          *
+ *        [max_iters][B][m] (first *iterations rows valid), host outputs     *
+ *        *iterations, converged[B] (0/1), residual[B] (float64).            *
+ *    nsw_sinkhorn_batch_*: the fixed-schedule, ranking-marginal form.       *
+ *    nsw_sinkhorn_backward_batch_* / _general_* replace                     *
+ *        _sinkhorn_backward_batch (reference sinkhorn.py:258-309)           *
+ *        -> grad_log_kernel [B][n][m]; _general_ takes the masses.          *
+ *    nsw_cost_from_policy_* replaces cost_from_policy (sinkhorn.py:176-188):*
+ *        cost = -epsilon log(plan) elementwise; NSW_ERR_DOMAIN unless every *
+ *        entry is > 0 and epsilon > 0.                                      *
  * ------------------------------------------------------------------------ */
+nsw_status nsw_sinkhorn_solve_batch_f64(const double* log_kernel, const double* row, const double* col,
+                                        const double* log_v_init, int32_t B, int32_t n, int32_t m,
+                                        int32_t max_iters, double tol, double* plan, double* log_u,
+                                        double* log_v, double* log_v_hist, int32_t* iterations,
+                                        int32_t* converged, double* residual, void* stream);
+nsw_status nsw_sinkhorn_solve_batch_f32(const float* log_kernel, const float* row, const float* col,
+                                        const float* log_v_init, int32_t B, int32_t n, int32_t m,
+                                        int32_t max_iters, double tol, float* plan, float* log_u,
+                                        float* log_v, float* log_v_hist, int32_t* iterations,
+                                        int32_t* converged, double* residual, void* stream);
 nsw_status nsw_sinkhorn_batch_f64(const double* log_kernel, const double* log_v_init, int32_t B,
                                   int32_t n, int32_t m, int32_t iters, double* plan, double* log_u,
                                   double* log_v, double* log_v_hist, void* stream);
@@ -218,6 +237,20 @@ nsw_status nsw_sinkhorn_backward_batch_f32(const float* log_kernel, const float*
                                            const float* plan, const float* log_u_final, int32_t B,
                                            int32_t n, int32_t m, int32_t iters,
                                            float* grad_log_kernel, void* stream);
+nsw_status nsw_sinkhorn_backward_general_f64(const double* log_kernel, const double* row, const double* col,
+                                             const double* log_v_hist, const double* log_v_init,
+                                             const double* grad_plan, const double* plan,
+                                             const double* log_u_final, int32_t B, int32_t n, int32_t m,
+                                             int32_t iters, double* grad_log_kernel, void* stream);
+nsw_status nsw_sinkhorn_backward_general_f32(const float* log_kernel, const float* row, const float* col,
+                                             const float* log_v_hist, const float* log_v_init,
+                                             const float* grad_plan, const float* plan,
+                                             const float* log_u_final, int32_t B, int32_t n, int32_t m,
+                                             int32_t iters, float* grad_log_kernel, void* stream);
+nsw_status nsw_cost_from_policy_f64(const double* plan, size_t count, double epsilon, double* cost,
+                                    void* stream);
+nsw_status nsw_cost_from_policy_f32(const float* plan, size_t count, double epsilon, float* cost,
+                                    void* stream);
 
 /* Whether a (dtype, n, m, iters) problem has a compiled tile variant. */
 int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);

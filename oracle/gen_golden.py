@@ -224,11 +224,53 @@ def case_metrics():
     np.savez(os.path.join(OUT, "metrics.npz"), **out)
 
 
+def case_api():
+    """Per-user API with general marginals (sinkhorn.py:85-188): the
+    reference's sinkhorn_solve / sinkhorn_backward / cost_from_policy and a
+    tolerance-mode _sinkhorn_batch over a small batch; pins the oracle's
+    general-marginal forward/backward against them bit-for-bit."""
+    from nswrank.sinkhorn import Marginals, cost_from_policy, sinkhorn_backward, sinkhorn_solve
+    rng = np.random.default_rng(21)
+    n, m = 23, 7
+    row = rng.uniform(0.5, 2.0, n)
+    col = rng.uniform(0.5, 2.0, m)
+    col *= row.sum() / col.sum()
+    cost = rng.normal(0.0, 1.0, (n, m))
+    cfg = nswrank.SolverConfig(epsilon=0.2, sinkhorn_tol=1e-7, sinkhorn_max_iters=400)
+    mg = Marginals(row, col)
+    plan, st = sinkhorn_solve(cost, mg, cfg)
+    gp = rng.normal(0.0, 1.0, (n, m))
+    grad = sinkhorn_backward(st, gp)
+    # pin the oracle (same arithmetic, general masses)
+    lk = -cost / cfg.epsilon
+    fw = orc.sinkhorn_forward(lk[None], np.log(row), np.log(col), row, col, cfg.sinkhorn_tol,
+                              cfg.sinkhorn_max_iters, np.zeros((1, m)))
+    assert fw.iterations == st.iterations_used and np.array_equal(fw.plan[0], plan)
+    g_or = orc.sinkhorn_backward(lk[None], np.log(row), np.log(col), fw.hist, np.zeros((1, m)), gp[None],
+                                 np.exp(fw.log_u[0][:, None] + lk + fw.log_v[0][None, :])[None],
+                                 fw.log_u) / (-cfg.epsilon)
+    assert np.array_equal(g_or[0], grad), np.abs(g_or[0] - grad).max()
+    # a lock-step batch in tolerance mode with the ranking marginals
+    B, nb, mb = 5, 30, 6
+    lkb = rng.normal(0.0, 3.0, (B, nb, mb))
+    lvb = rng.normal(0.0, 0.3, (B, mb))
+    mr = Marginals.for_shape(nb, mb)
+    rb = ref_sink._sinkhorn_batch(lkb, np.log(mr.row), np.log(mr.col), mr.row, mr.col, 1e-6, 300, lvb, True)
+    pol = rng.random((3, nb, mb)) + 0.01
+    np.savez(os.path.join(OUT, "api_small.npz"), cost=cost, row=row, col=col, eps=cfg.epsilon, tol=cfg.sinkhorn_tol,
+             max_iters=cfg.sinkhorn_max_iters, plan=plan, log_u=st.log_u, log_v=st.log_v,
+             iterations=st.iterations_used, converged=st.converged, residual=st.final_residual, grad_plan=gp,
+             grad_cost=grad, b_log_kernel=lkb, b_lvi=lvb, b_plan=rb.plan, b_log_u=rb.log_u, b_log_v=rb.log_v,
+             b_hist=rb.log_v_hist, b_iterations=rb.iterations, b_converged=rb.converged, b_residual=rb.residual,
+             policy=pol, policy_cost=cost_from_policy(pol, 0.3))
+    print(f"api: solve {st.iterations_used} iterations (converged {st.converged}), batch {rb.iterations}")
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    which = sys.argv[1:] or ["ops", "cfg0", "tol", "cfg1", "metrics"]
+    which = sys.argv[1:] or ["ops", "cfg0", "tol", "cfg1", "metrics", "api"]
     for w in which:
         t = time.time()
         {"ops": case_ops, "cfg0": case_cfg0, "tol": case_tolerance_desk, "cfg1": case_cfg1_slice,
-         "metrics": case_metrics}[w]()
+         "metrics": case_metrics, "api": case_api}[w]()
         print(f"  {w}: {time.time() - t:.1f}s")

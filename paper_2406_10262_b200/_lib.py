@@ -79,6 +79,16 @@ SIGNATURES = {
     "nsw_top_positions_f64": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "nsw_policy_metrics_f32": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
     "nsw_policy_metrics_f64": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
+    "nsw_sinkhorn_solve_batch_f64": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_double, _vp, _vp,
+                                               _vp, _vp, C.POINTER(_i32), C.POINTER(_i32), _dp, _vp]),
+    "nsw_sinkhorn_solve_batch_f32": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_double, _vp, _vp,
+                                               _vp, _vp, C.POINTER(_i32), C.POINTER(_i32), _dp, _vp]),
+    "nsw_sinkhorn_backward_general_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
+                                                    _vp, _vp]),
+    "nsw_sinkhorn_backward_general_f32": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32,
+                                                    _vp, _vp]),
+    "nsw_cost_from_policy_f64": (C.c_int, [_vp, C.c_size_t, C.c_double, _vp, _vp]),
+    "nsw_cost_from_policy_f32": (C.c_int, [_vp, C.c_size_t, C.c_double, _vp, _vp]),
     "nsw_sinkhorn_batch_f64": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_batch_f32": (C.c_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp]),
     "nsw_sinkhorn_backward_batch_f64": (C.c_int, [_vp, _vp, _vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp]),
