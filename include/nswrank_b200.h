@@ -192,6 +192,28 @@ nsw_status nsw_policy_metrics_f32(const float* X, const float* rel, const double
 nsw_status nsw_policy_metrics_f64(const double* X, const double* rel, const double* expo, int32_t U, int32_t n,
                                   int32_t m, double threshold, double* out_host, void* stream);
 
+/* Building blocks of the ascent as standalone device ops (reference
+ * solver.py:46-122), for callers that compose their own loop:
+ *   nsw_policy_impact_*     Imp_i = sum_{u,k<m-1} r_ui e_k x_uik -> host imp[n]
+ *   nsw_welfare_gradient_*  grad [U][n][m] = r_ui e_k / Imp_i (0 at the dummy)
+ *   nsw_adam_update_*       one Adam ascent step in place on count entries,
+ *                           bias1/bias2 = 1 - beta^step as the caller computes
+ *                           them; IEEE operations in the reference's order. */
+nsw_status nsw_policy_impact_f32(const float* X, const float* rel, const double* expo, int32_t U, int32_t n,
+                                 int32_t m, double* imp_host, void* stream);
+nsw_status nsw_policy_impact_f64(const double* X, const double* rel, const double* expo, int32_t U, int32_t n,
+                                 int32_t m, double* imp_host, void* stream);
+nsw_status nsw_welfare_gradient_f32(const float* rel, const double* expo, const double* imp, int32_t U,
+                                    int32_t n, int32_t m, float* grad, void* stream);
+nsw_status nsw_welfare_gradient_f64(const double* rel, const double* expo, const double* imp, int32_t U,
+                                    int32_t n, int32_t m, double* grad, void* stream);
+nsw_status nsw_adam_update_f32(float* params, const float* grads, float* adam_m, float* adam_v, size_t count,
+                               double lr, double beta1, double beta2, double eps, double bias1, double bias2,
+                               void* stream);
+nsw_status nsw_adam_update_f64(double* params, const double* grads, double* adam_m, double* adam_v,
+                               size_t count, double lr, double beta1, double beta2, double eps, double bias1,
+                               double bias2, void* stream);
+
 /* ------------------------------------------------------------------------ *
  * 3. Inner operator seam (device pointers; one CTA per batch element).     *
  *    nsw_sinkhorn_solve_batch_* replaces _sinkhorn_batch (reference         *

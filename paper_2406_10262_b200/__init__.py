@@ -11,9 +11,11 @@ __version__ = "0.1.0"
 _EXPORTS = {
     "core": ("ProblemShape", "RelevanceMatrix", "ExposureModel", "RankingPolicy", "SolverConfig",
              "ShapeError", "DomainError", "StateError", "SolverError", "RELEVANCE_FLOOR", "uniform_policy"),
-    "solver": ("SolveTrace", "DeviceOptions", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError"),
+    "solver": ("SolveTrace", "DeviceOptions", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError",
+               "impact", "nsw_objective", "nsw_gradient_wrt_policy", "AdamState", "adam_update"),
     "data": ("exposure_model", "make_instance", "BASELINE_CONFIGS"),
-    "sinkhorn": ("sinkhorn_batch", "sinkhorn_backward_batch"),
+    "sinkhorn": ("sinkhorn_batch", "sinkhorn_backward_batch", "sinkhorn_batch_solve", "Marginals", "SinkhornState",
+                 "sinkhorn_solve", "sinkhorn_backward", "cost_from_policy"),
     "ranking": ("top_positions",),
     "metrics": ("user_utility", "mean_max_envy", "items_better_off", "items_worse_off", "policy_metrics"),
     "distributed": ("solve_fair_ranking_distributed", "shard_users"),

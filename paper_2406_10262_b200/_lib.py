@@ -77,6 +77,12 @@ SIGNATURES = {
     "nsw_solver_tol_decide": (C.c_int, [_vp, _vp, C.POINTER(_i32)]),
     "nsw_top_positions_f32": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
     "nsw_top_positions_f64": (C.c_int, [_vp, _i32, _i32, _i32, _vp, _vp]),
+    "nsw_policy_impact_f32": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, _dp, _vp]),
+    "nsw_policy_impact_f64": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, _dp, _vp]),
+    "nsw_welfare_gradient_f32": (C.c_int, [_vp, _dp, _dp, _i32, _i32, _i32, _vp, _vp]),
+    "nsw_welfare_gradient_f64": (C.c_int, [_vp, _dp, _dp, _i32, _i32, _i32, _vp, _vp]),
+    "nsw_adam_update_f32": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t] + [C.c_double] * 6 + [_vp]),
+    "nsw_adam_update_f64": (C.c_int, [_vp, _vp, _vp, _vp, C.c_size_t] + [C.c_double] * 6 + [_vp]),
     "nsw_policy_metrics_f32": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
     "nsw_policy_metrics_f64": (C.c_int, [_vp, _vp, _dp, _i32, _i32, _i32, C.c_double, _dp, _vp]),
     "nsw_sinkhorn_solve_batch_f64": (C.c_int, [_vp, _vp, _vp, _vp, _i32, _i32, _i32, _i32, C.c_double, _vp, _vp,

@@ -197,10 +197,147 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   return status;
 }
 
+// Imp only (reference solver.py:46-53): allocation masses + two-level sums
+template <typename S>
+nsw_status policy_impact(const void* X, const void* rel, const double* expo_host, int32_t U, int32_t n, int32_t m,
+                         double* imp_host, void* stream) {
+  if (!X || !rel || !expo_host || !imp_host) return NSW_ERR_ARG;
+  if (U <= 0 || n <= 0 || m < 2) return NSW_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const size_t cells = size_t(U) * n;
+  const int chunks = std::max(1, std::min(U, (148 * 4 * 128 + n - 1) / n));
+  double* buf = nullptr;   // e[m] | A[U n] | imp[n] | unif[n] | pa, pb [chunks n]
+  const size_t words = size_t(m) + cells + 2 * size_t(n) + 2 * size_t(chunks) * n;
+  if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  double* e = buf;
+  double* A = e + m;
+  double* imp = A + cells;
+  double* unif = imp + n;
+  double* pa = unif + n;
+  double* pb = pa + size_t(chunks) * n;
+  nsw_status status = NSW_OK;
+  if (cudaMemcpyAsync(e, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    status = NSW_ERR_CUDA;
+  } else {
+    alloc_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
+    impact_partial_kernel<S><<<dim3((n + 127) / 128, chunks), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n,
+                                                                             chunks, pa, pb);
+    impact_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(pa, pb, n, chunks, 0.0, imp, unif);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(imp_host, imp, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      status = NSW_ERR_CUDA;
+  }
+  cudaFreeAsync(buf, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) status = NSW_ERR_CUDA;
+  return status;
+}
+
+// grad[u][i][k] = r_ui e_k / Imp_i for k < m-1, 0 at the dummy (solver.py:68-90)
+template <typename S>
+__global__ void welfare_gradient_kernel(const S* __restrict__ rel, const double* __restrict__ e,
+                                        const double* __restrict__ imp, int U, int n, int m, S* __restrict__ grad) {
+  const size_t total = size_t(U) * n * m;
+  for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < total; q += size_t(gridDim.x) * blockDim.x) {
+    const int k = int(q % m);
+    const size_t ui = q / m;
+    const int i = int(ui % n);
+    grad[q] = k < m - 1 ? S((double(rel[ui]) * e[k]) / imp[i]) : S(0);
+  }
+}
+
+template <typename S>
+nsw_status welfare_gradient(const void* rel, const double* expo_host, const double* imp_host, int32_t U, int32_t n,
+                            int32_t m, void* grad, void* stream) {
+  if (!rel || !expo_host || !imp_host || !grad) return NSW_ERR_ARG;
+  if (U <= 0 || n <= 0 || m < 2) return NSW_ERR_SHAPE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* buf = nullptr;
+  if (cudaMallocAsync((void**)&buf, (size_t(m) + n) * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  nsw_status status = NSW_OK;
+  if (cudaMemcpyAsync(buf, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(buf + m, imp_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    status = NSW_ERR_CUDA;
+  } else {
+    welfare_gradient_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(rel), buf, buf + m, U, n, m,
+                                                        static_cast<S*>(grad));
+    if (cudaGetLastError() != cudaSuccess) status = NSW_ERR_CUDA;
+  }
+  cudaFreeAsync(buf, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) status = NSW_ERR_CUDA;
+  return status;
+}
+
+// One Adam ascent step in place (solver.py:105-122), the reference's
+// operation order; bias corrections bc1 = 1 - b1^step, bc2 = 1 - b2^step
+// come from the host exactly as Python computes them.
+// IEEE round-to-nearest operations, never contracted into FMAs (numpy order)
+__device__ __forceinline__ double rmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double radd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rdiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double rsqrt_(double a) { return __dsqrt_rn(a); }
+__device__ __forceinline__ float rmul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float radd(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float rdiv(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float rsqrt_(float a) { return __fsqrt_rn(a); }
+
+template <typename S>
+__global__ void adam_kernel(S* __restrict__ p, const S* __restrict__ g, S* __restrict__ m1, S* __restrict__ v1,
+                            size_t count, double lr, double b1, double b2, double eps, double bc1, double bc2) {
+  for (size_t q = blockIdx.x * size_t(blockDim.x) + threadIdx.x; q < count; q += size_t(gridDim.x) * blockDim.x) {
+    const S gg = g[q];
+    const S mm = radd(rmul(S(b1), m1[q]), rmul(S(1.0 - b1), gg));
+    const S vv = radd(rmul(S(b2), v1[q]), rmul(rmul(S(1.0 - b2), gg), gg));
+    m1[q] = mm;
+    v1[q] = vv;
+    const S mh = rdiv(mm, S(bc1));
+    const S vh = rdiv(vv, S(bc2));
+    p[q] = radd(p[q], rdiv(rmul(S(lr), mh), radd(rsqrt_(vh), S(eps))));
+  }
+}
+
 }  // namespace
 }  // namespace nsw
 
 extern "C" {
+
+nsw_status nsw_policy_impact_f32(const float* X, const float* rel, const double* expo, int32_t U, int32_t n,
+                                 int32_t m, double* imp, void* stream) {
+  return nsw::policy_impact<float>(X, rel, expo, U, n, m, imp, stream);
+}
+
+nsw_status nsw_policy_impact_f64(const double* X, const double* rel, const double* expo, int32_t U, int32_t n,
+                                 int32_t m, double* imp, void* stream) {
+  return nsw::policy_impact<double>(X, rel, expo, U, n, m, imp, stream);
+}
+
+nsw_status nsw_welfare_gradient_f32(const float* rel, const double* expo, const double* imp, int32_t U, int32_t n,
+                                    int32_t m, float* grad, void* stream) {
+  return nsw::welfare_gradient<float>(rel, expo, imp, U, n, m, grad, stream);
+}
+
+nsw_status nsw_welfare_gradient_f64(const double* rel, const double* expo, const double* imp, int32_t U, int32_t n,
+                                    int32_t m, double* grad, void* stream) {
+  return nsw::welfare_gradient<double>(rel, expo, imp, U, n, m, grad, stream);
+}
+
+nsw_status nsw_adam_update_f32(float* params, const float* grads, float* adam_m, float* adam_v, size_t count,
+                               double lr, double beta1, double beta2, double eps, double bias1, double bias2,
+                               void* stream) {
+  if (!params || !grads || !adam_m || !adam_v) return NSW_ERR_ARG;
+  nsw::adam_kernel<float><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
+                                                                     beta2, eps, bias1, bias2);
+  return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
+}
+
+nsw_status nsw_adam_update_f64(double* params, const double* grads, double* adam_m, double* adam_v, size_t count,
+                               double lr, double beta1, double beta2, double eps, double bias1, double bias2,
+                               void* stream) {
+  if (!params || !grads || !adam_m || !adam_v) return NSW_ERR_ARG;
+  nsw::adam_kernel<double><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
+                                                                      beta2, eps, bias1, bias2);
+  return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
+}
+
 
 nsw_status nsw_policy_metrics_f32(const float* X, const float* rel, const double* expo, int32_t U, int32_t n,
                                   int32_t m, double threshold, double* out, void* stream) {

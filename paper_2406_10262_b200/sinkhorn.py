@@ -37,7 +37,10 @@ def _to_dev(x, dtype):
     import torch
     if isinstance(x, torch.Tensor):
         return x.to(dtype=dtype).contiguous(), True
-    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda"), False
+    a = np.asarray(x)
+    if not a.flags.writeable or not a.flags.c_contiguous:
+        a = np.array(a, copy=True, order="C")
+    return torch.as_tensor(a, dtype=dtype, device="cuda"), False
 
 
 def _dtype_of(x):

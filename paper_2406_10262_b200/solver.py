@@ -354,3 +354,106 @@ def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOption
                        [float(x) for x in wall[:k]])
     # float32 solves verify finiteness on the device while widening the policy
     return RankingPolicy._adopt(pol, finite_checked=options.dtype == "float32"), trace
+
+
+# ---------------------------------------------------------------------------
+# Building blocks of the ascent as standalone device ops (reference
+# solver.py:46-122): the same names and semantics, for callers that compose
+# their own loop.  numpy in -> numpy out; CUDA torch tensors stay on device.
+# ---------------------------------------------------------------------------
+def _as_dev(x, dtype=None):
+    import torch
+    if isinstance(x, torch.Tensor):
+        t = x if dtype is None else x.to(dtype)
+        return t.to("cuda").contiguous(), True
+    a = np.asarray(x)
+    if dtype is None:
+        dtype = torch.float32 if a.dtype == np.float32 else torch.float64
+    if not a.flags.writeable or not a.flags.c_contiguous:
+        a = np.array(a, copy=True, order="C")
+    return torch.as_tensor(a, device="cuda").to(dtype), False
+
+
+def impact(policy, relevance, exposure) -> np.ndarray:
+    """Expected impact per item, Imp_i = sum_{u,k<m-1} r_ui e_k x_uik
+    (reference solver.py:46-53), float64 [n], computed on the device."""
+    import torch
+    x = policy if isinstance(policy, torch.Tensor) else getattr(policy, "values", policy)
+    X, _ = _as_dev(x)
+    R, _ = _as_dev(relevance if isinstance(relevance, torch.Tensor) else _values(relevance, "relevance"), X.dtype)
+    e = np.ascontiguousarray(getattr(exposure, "values", exposure), dtype=np.float64)
+    U, n, m = X.shape
+    if tuple(R.shape) != (U, n) or e.shape != (m - 1,):
+        raise ShapeError(f"relevance {tuple(R.shape)} / exposure {e.shape} do not match policy {tuple(X.shape)}")
+    out = np.zeros(n)
+    lib = _lib.load()
+    fn = lib.nsw_policy_impact_f32 if X.dtype == torch.float32 else lib.nsw_policy_impact_f64
+    check(fn(X.data_ptr(), R.data_ptr(), _lib.dptr(e), U, n, m, _lib.dptr(out),
+             torch.cuda.current_stream(X.device).cuda_stream), "impact")
+    return out
+
+
+def nsw_objective(impacts) -> float:
+    """Log Nash social welfare sum_i log Imp_i (reference solver.py:56-65); an
+    n-vector reduction, done on the host like the reference."""
+    imp = np.asarray(impacts, dtype=np.float64)
+    if imp.size == 0 or imp.min() <= 0.0:
+        raise DomainError("impacts must be strictly positive")
+    return float(np.log(imp).sum())
+
+
+def nsw_gradient_wrt_policy(policy, relevance, exposure):
+    """r_ui e_k / Imp_i at real positions, 0 at the dummy (reference
+    solver.py:68-90), computed on the device."""
+    import torch
+    x = policy if isinstance(policy, torch.Tensor) else getattr(policy, "values", policy)
+    imp = impact(x, relevance, exposure)
+    if imp.min() <= 0.0:
+        raise DomainError("impacts must be strictly positive to differentiate the welfare")
+    X, as_t = _as_dev(x)
+    R, _ = _as_dev(relevance if isinstance(relevance, torch.Tensor) else _values(relevance, "relevance"), X.dtype)
+    e = np.ascontiguousarray(getattr(exposure, "values", exposure), dtype=np.float64)
+    U, n, m = X.shape
+    grad = torch.empty_like(X)
+    lib = _lib.load()
+    fn = lib.nsw_welfare_gradient_f32 if X.dtype == torch.float32 else lib.nsw_welfare_gradient_f64
+    check(fn(R.data_ptr(), _lib.dptr(e), _lib.dptr(imp), U, n, m, grad.data_ptr(),
+             torch.cuda.current_stream(X.device).cuda_stream), "nsw_gradient_wrt_policy")
+    return grad if as_t else grad.cpu().numpy()
+
+
+@dataclass
+class AdamState:
+    """First/second moment accumulators (reference solver.py:92-102)."""
+
+    m: object
+    v: object
+    step: int = 0
+
+    @classmethod
+    def zeros(cls, shape) -> "AdamState":
+        return cls(m=np.zeros(shape), v=np.zeros(shape), step=0)
+
+
+def adam_update(params, grads, state: AdamState, config):
+    """One Adam ascent step (reference solver.py:105-122) on the device:
+    returns (updated params, new AdamState); the inputs are not modified."""
+    import torch
+    P, as_t = _as_dev(params)
+    G, _ = _as_dev(grads, P.dtype)
+    Mm, _ = _as_dev(state.m, P.dtype)
+    Vv, _ = _as_dev(state.v, P.dtype)
+    if G.shape != P.shape or Mm.shape != P.shape or Vv.shape != P.shape:
+        raise ShapeError("params, grads and state must share one shape")
+    P, Mm, Vv = P.clone(), Mm.clone(), Vv.clone()
+    step = state.step + 1
+    b1, b2 = config.adam_beta1, config.adam_beta2
+    lib = _lib.load()
+    fn = lib.nsw_adam_update_f32 if P.dtype == torch.float32 else lib.nsw_adam_update_f64
+    check(fn(P.data_ptr(), G.data_ptr(), Mm.data_ptr(), Vv.data_ptr(), P.numel(), config.adam_lr, b1, b2,
+             config.adam_eps, 1.0 - b1 ** step, 1.0 - b2 ** step, torch.cuda.current_stream(P.device).cuda_stream),
+          "adam_update")
+    torch.cuda.synchronize(P.device)
+    if as_t:
+        return P, AdamState(m=Mm, v=Vv, step=step)
+    return P.cpu().numpy(), AdamState(m=Mm.cpu().numpy(), v=Vv.cpu().numpy(), step=step)

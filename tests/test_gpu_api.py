@@ -65,3 +65,33 @@ def test_cost_from_policy_theorem1_map(golden):
         cost_from_policy(bad, 0.3)
     with pytest.raises(DomainError):
         cost_from_policy(g["policy"], 0.0)
+
+
+def test_ascent_building_blocks_match_oracle(golden):
+    """impact / nsw_objective / nsw_gradient_wrt_policy / adam_update on the
+    device vs the oracle (pinned bit-exact to the reference)."""
+    from oracle import nsw_oracle as orc
+    from paper_2406_10262_b200 import (AdamState, SolverConfig, adam_update, impact, nsw_gradient_wrt_policy,
+                                       nsw_objective)
+    g = golden("cfg0_fixed")
+    rel, expo, x = g["relevance"], g["exposure"], g["policy"]
+    imp_d = impact(x, rel, expo)
+    imp_o = orc.impact(rel, expo, x)
+    assert np.abs(imp_d / imp_o - 1).max() <= 1e-13
+    assert nsw_objective(imp_d) == pytest.approx(float(np.log(imp_o).sum()), rel=1e-14)
+    gd = nsw_gradient_wrt_policy(x, rel, expo)
+    go = np.zeros_like(x)
+    orc.welfare_gradient(rel, expo, imp_d, go)   # same impacts: the division is elementwise-exact
+    assert np.array_equal(gd, go)
+    cfg = SolverConfig()
+    rng = np.random.default_rng(4)
+    p0, g0 = rng.normal(size=(5, 7, 3)), rng.normal(size=(5, 7, 3))
+    st = AdamState.zeros(p0.shape)
+    p1, st1 = adam_update(p0, g0, st, cfg)
+    p2, st2 = adam_update(p1, g0 * 0.5, st1, cfg)
+    q1, m1, v1, s1 = orc.adam_ascent(p0, g0, np.zeros_like(p0), np.zeros_like(p0), 0, cfg.adam_lr, cfg.adam_beta1,
+                                     cfg.adam_beta2, cfg.adam_eps)
+    q2, m2, v2, s2 = orc.adam_ascent(q1, g0 * 0.5, m1, v1, s1, cfg.adam_lr, cfg.adam_beta1, cfg.adam_beta2,
+                                     cfg.adam_eps)
+    assert st2.step == s2 == 2
+    assert np.array_equal(p2, q2) and np.array_equal(st2.m, m2) and np.array_equal(st2.v, v2)
