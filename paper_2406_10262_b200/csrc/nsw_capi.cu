@@ -215,7 +215,7 @@ nsw_status download_converted(int dtype, const void* src, double* dst, size_t co
     CUDA_TRY(cudaMallocAsync((void**)&wide, count * 8 + 16, st));
     unsigned* bad = reinterpret_cast<unsigned*>(wide + count);   // one word past the values
     CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
-    widen_kernel<<<148 * 4, 256, 0, st>>>(static_cast<const float*>(src), wide, count, bad);
+    widen_kernel<<<sm_count() * 4, 256, 0, st>>>(static_cast<const float*>(src), wide, count, bad);
     cudaError_t ce = cudaGetLastError();
     unsigned bad_h = 0;
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(dst, wide, count * 8, cudaMemcpyDeviceToHost, st);
@@ -465,7 +465,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->expo_d, size_t(m) * 8);
   ALLOC(s->partial, size_t(users_local) * n * 8);
   // impact reduction: ~2 CTAs per SM of (8 items x user chunk)
-  s->imp_chunks = std::max(1, std::min(std::min(users_local, 64), (2 * 148 * IMP_ITEMS + n - 1) / n));
+  s->imp_chunks = std::max(1, std::min(std::min(users_local, 64), (2 * sm_count() * IMP_ITEMS + n - 1) / n));
   ALLOC(s->split, size_t(s->imp_chunks) * n * 8);
   ALLOC(s->own_imp_local, size_t(n + 1) * 8);
   ALLOC(s->own_imp_all, size_t(world) * (n + 1) * 8);
@@ -931,12 +931,12 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
   for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
   for (int i = 0; i < steps; ++i) {
     if (flush_l2) {
-      flush_kernel<<<148 * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
+      flush_kernel<<<sm_count() * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
       CUDA_TRY(cudaGetLastError());
       // drop the flush buffer's dirty lines without writing them back: the
       // timed step starts from a cold, clean L2 instead of paying the
       // flush's write-backs
-      discard_kernel<<<148 * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
+      discard_kernel<<<sm_count() * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
       CUDA_TRY(cudaGetLastError());
     }
     CUDA_TRY(cudaEventRecord(ev[3 * i], s->stream));

@@ -262,6 +262,18 @@ __device__ __forceinline__ void sts_vec(S* dst, const S (&src)[M]) {
   }
 }
 
+// Host: SM count of the current device (grid sizing of the streaming
+// kernels: a few CTAs per SM), cached per host thread.
+inline int sm_count() {
+  thread_local int dev = -1, sms = 148;
+  int d = 0;
+  if (cudaGetDevice(&d) == cudaSuccess && d != dev) {
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d) != cudaSuccess) sms = 148;
+    dev = d;
+  }
+  return sms;
+}
+
 // Asynchronous global -> shared copy of one scalar (cp.async, Ampere-style);
 // valid == false zero-fills the destination without reading the source.
 template <typename S>

@@ -15,6 +15,7 @@
 #include <cstring>
 
 #include "../../include/nswrank_b200.h"
+#include "nsw_device.cuh"
 
 namespace nsw {
 namespace {
@@ -133,7 +134,7 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t cells = size_t(U) * n;
   // user chunks of the impact sums: ~4 CTAs of 128 items per SM
-  const int chunks = std::max(1, std::min(U, (148 * 4 * 128 + n - 1) / n));
+  const int chunks = std::max(1, std::min(U, (sm_count() * 4 * 128 + n - 1) / n));
   double* buf = nullptr;   // e[m] | A[U n] | cross[n n] | imp[n] | unif[n] | envy[n] | out[4] | pa, pb [chunks n]
   const size_t words = size_t(m) + cells + size_t(n) * n + 3 * size_t(n) + 4 + 2 * size_t(chunks) * n;
   {
@@ -162,7 +163,7 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   if (cudaMemcpyAsync(e, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
     status = NSW_ERR_CUDA;
   } else {
-    alloc_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
+    alloc_kernel<S><<<sm_count() * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
     impact_partial_kernel<S><<<dim3((n + 127) / 128, chunks), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n,
                                                                              chunks, pa, pb);
     impact_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(pa, pb, n, chunks, esum / n, imp, unif);
@@ -174,7 +175,7 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
     } else {
       // widen R for DGEMM (float64 products, as the reference's numpy matmul)
       if (cudaMallocAsync((void**)&Rd, cells * sizeof(double), st) != cudaSuccess) status = NSW_ERR_CUDA;
-      else widen_to_f64<<<148 * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
+      else widen_to_f64<<<sm_count() * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
     }
     if (status == NSW_OK && (h = cublas_handle()) == nullptr) status = NSW_ERR_CUDA;
     if (status == NSW_OK && cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
@@ -205,7 +206,7 @@ nsw_status policy_impact(const void* X, const void* rel, const double* expo_host
   if (U <= 0 || n <= 0 || m < 2) return NSW_ERR_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const size_t cells = size_t(U) * n;
-  const int chunks = std::max(1, std::min(U, (148 * 4 * 128 + n - 1) / n));
+  const int chunks = std::max(1, std::min(U, (sm_count() * 4 * 128 + n - 1) / n));
   double* buf = nullptr;   // e[m] | A[U n] | imp[n] | unif[n] | pa, pb [chunks n]
   const size_t words = size_t(m) + cells + 2 * size_t(n) + 2 * size_t(chunks) * n;
   if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
@@ -219,7 +220,7 @@ nsw_status policy_impact(const void* X, const void* rel, const double* expo_host
   if (cudaMemcpyAsync(e, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
     status = NSW_ERR_CUDA;
   } else {
-    alloc_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
+    alloc_kernel<S><<<sm_count() * 8, 256, 0, st>>>(static_cast<const S*>(X), e, U, n, m, A);
     impact_partial_kernel<S><<<dim3((n + 127) / 128, chunks), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n,
                                                                              chunks, pa, pb);
     impact_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(pa, pb, n, chunks, 0.0, imp, unif);
@@ -258,7 +259,7 @@ nsw_status welfare_gradient(const void* rel, const double* expo_host, const doub
       cudaMemcpyAsync(buf + m, imp_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
     status = NSW_ERR_CUDA;
   } else {
-    welfare_gradient_kernel<S><<<148 * 8, 256, 0, st>>>(static_cast<const S*>(rel), buf, buf + m, U, n, m,
+    welfare_gradient_kernel<S><<<sm_count() * 8, 256, 0, st>>>(static_cast<const S*>(rel), buf, buf + m, U, n, m,
                                                         static_cast<S*>(grad));
     if (cudaGetLastError() != cudaSuccess) status = NSW_ERR_CUDA;
   }
@@ -324,7 +325,7 @@ nsw_status nsw_adam_update_f32(float* params, const float* grads, float* adam_m,
                                double lr, double beta1, double beta2, double eps, double bias1, double bias2,
                                void* stream) {
   if (!params || !grads || !adam_m || !adam_v) return NSW_ERR_ARG;
-  nsw::adam_kernel<float><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
+  nsw::adam_kernel<float><<<nsw::sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
                                                                      beta2, eps, bias1, bias2);
   return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
 }
@@ -333,7 +334,7 @@ nsw_status nsw_adam_update_f64(double* params, const double* grads, double* adam
                                double lr, double beta1, double beta2, double eps, double bias1, double bias2,
                                void* stream) {
   if (!params || !grads || !adam_m || !adam_v) return NSW_ERR_ARG;
-  nsw::adam_kernel<double><<<148 * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
+  nsw::adam_kernel<double><<<nsw::sm_count() * 8, 256, 0, (cudaStream_t)stream>>>(params, grads, adam_m, adam_v, count, lr, beta1,
                                                                       beta2, eps, bias1, bias2);
   return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
 }

@@ -476,7 +476,7 @@ nsw_status cost_from_policy(const S* x, size_t count, double eps, S* out, void* 
   unsigned hbad = 0;
   if (cudaMallocAsync((void**)&bad, sizeof(unsigned), st) != cudaSuccess) return NSW_ERR_CUDA;
   cudaMemsetAsync(bad, 0, sizeof(unsigned), st);
-  cost_from_policy_op<S><<<148 * 4, 256, 0, st>>>(x, count, S(-eps), out, bad);
+  cost_from_policy_op<S><<<sm_count() * 4, 256, 0, st>>>(x, count, S(-eps), out, bad);
   cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(bad, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) return NSW_ERR_CUDA;
