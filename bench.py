@@ -234,8 +234,17 @@ def run_ours(a):
     import torch
     world, rank, local = _dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or a.sharded:
+        import socket
         import torch.distributed as dist
+        if world == 1:   # --sharded outside torchrun: a 1-rank group
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            if "MASTER_PORT" not in os.environ:
+                with socket.socket() as sk:
+                    sk.bind(("127.0.0.1", 0))
+                    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2406_10262_b200 import DeviceOptions, ExposureModel, ProblemShape, RelevanceMatrix, SolverConfig
     from paper_2406_10262_b200.solver import DeviceSolver, solve_fair_ranking
@@ -252,16 +261,17 @@ def run_ours(a):
                         grad_threshold=1e-300)
     peaks, peaks_kind = _peaks()
 
-    if world == 1:
+    if world == 1 and not a.sharded:
         solver = DeviceSolver(rel, expo, n, m, scfg, opts)
         solver.run(a.warmup)
         torch.cuda.synchronize()
+        launches0 = solver.launch_count()
         with ClockSampler(local) as cs:
             ms_total, ms_fused = solver.time_steps(a.steps, flush_l2=True)
         torch.cuda.synchronize()
+        launches = solver.launch_count() - launches0   # our kernels in the timed steps
         phase, steps_done, err = solver.status()
         variant = solver.variant()
-        launches = 3 * a.steps
         solver.close()
         users_local = U
     else:
@@ -272,21 +282,25 @@ def run_ours(a):
             sa.step()
         torch.cuda.synchronize()
         dist.barrier()
-        ev0 = torch.cuda.Event(enable_timing=True)
-        ev1 = torch.cuda.Event(enable_timing=True)
+        # every step timed on the solver's stream between CUDA events, the L2
+        # evicted (outside the events) before each one, as in the 1-GPU path
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
         with ClockSampler(local) as cs:
-            ev0.record(sa.stream)
-            for _ in range(a.steps):
+            for e0, e1 in evs:
+                sa.solver.flush_l2(sa.stream.cuda_stream)
+                e0.record(sa.stream)
                 sa.step()
-            ev1.record(sa.stream)
+                e1.record(sa.stream)
             torch.cuda.synchronize()
         dist.barrier()
-        t = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+        t = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in evs)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
         ms_fused = float("nan")
         variant = sa.solver.variant()
-        launches = 3 * a.steps
+        # the step replays a torch-captured graph: main (+ tail) fused launch,
+        # impact reduction and finalize (our kernels) around the NCCL all-gather
+        launches = a.steps * ((2 if variant.get("tail_users", 0) else 1) + 2)
         users_local = sa.stop - sa.start
         sa.solver.close()
 
@@ -301,7 +315,7 @@ def run_ours(a):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if a.dtype == "float32" else "f64",
             "data": "synthetic (BASELINE generator, seed 0)",
             "config": {"workload": f"{a.config}: U={U} I={n} m={m} eps={cfg.epsilon} T_in={T} (fixed schedule)",
-                       "users_per_gpu": users_local, "l2": "flushed between timed steps (1 GiB write)",
+                       "users_per_gpu": users_local, "l2": "flushed between timed steps (1 GiB write, then discard of those lines)",
                        "tile": variant},
             "sinkhorn_cell_updates_per_s": cell_updates / (ms_total / 1e3),
             "gpu_launches": launches, "clocks": clocks}
@@ -334,7 +348,30 @@ def run_ours(a):
         line["sinkhorn_cell_updates_per_s_fused_kernel"] = cell_updates / (ms_fused / 1e3)
 
     # e2e: the public API with host buffers, K outer steps, copies included
-    if world == 1 and not a.no_e2e:
+    if (world > 1 or a.sharded) and not a.no_e2e:
+        # e2e at N GPUs: the SPMD drop-in with host float64 arrays on every rank
+        from paper_2406_10262_b200.distributed import solve_fair_ranking_distributed
+        ecfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=a.steps,
+                            grad_threshold=1e-300)
+        R, E, S = RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m)
+        solve_fair_ranking_distributed(R, E, S, SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T,
+                                                             outer_max_iters=2, grad_threshold=1e-300), opts,
+                                       gather_policy=False)   # warm
+        dist.barrier()
+        t0 = time.perf_counter()
+        pol, tr = solve_fair_ranking_distributed(R, E, S, ecfg, opts, gather_policy=False)
+        t_local = time.perf_counter() - t0
+        tt = torch.tensor([t_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+        es = 4 if a.dtype == "float32" else 8
+        line["e2e"] = {"value": len(tr) / t_e2e, "unit": "outer_iters/s",
+                       "h2d_bytes_per_step": (users_local * n * es + 2 * m * es + n * 8) / a.steps,
+                       "d2h_bytes_per_step": (users_local * n * m * es + a.steps * 8 * 3) / a.steps,
+                       "what": f"solve_fair_ranking_distributed(host float64 arrays) on {world} rank(s), "
+                               f"{a.steps} outer steps, each rank's policy block returned; max over ranks",
+                       "seconds": t_e2e}
+    if world == 1 and not a.sharded and not a.no_e2e:
         ecfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=a.steps,
                             grad_threshold=1e-300)
         R, E, S = RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m)
@@ -357,7 +394,7 @@ def run_ours(a):
         line["cpu_baseline"].pop("seconds_per_step", None)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or a.sharded:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
@@ -372,6 +409,8 @@ def main(argv=None):
     ap.add_argument("--dtype", default=None, choices=["float32", "float64"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the multi-GPU driver (ShardedAscent over torch.distributed) even at N=1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     # experiment knobs (not used by the driver): override |U|, inner iterations, tile variant
     ap.add_argument("--users", type=int, default=None)

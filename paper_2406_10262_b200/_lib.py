@@ -72,6 +72,7 @@ SIGNATURES = {
     "nsw_solver_phase_times": (C.c_int, [_vp, C.POINTER(C.c_uint64), _i32]),
     "nsw_solver_top_positions": (C.c_int, [_vp, C.POINTER(_i32)]),
     "nsw_solver_metrics": (C.c_int, [_vp, C.c_double, _dp]),
+    "nsw_solver_flush_l2": (C.c_int, [_vp, _vp]),
     "nsw_solver_bind_tol_exchange": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_local": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_decide": (C.c_int, [_vp, _vp, C.POINTER(_i32)]),

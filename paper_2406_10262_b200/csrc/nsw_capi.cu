@@ -918,51 +918,94 @@ nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT
 
 int32_t nsw_solver_tail_users(nsw_solver* s) { return s ? s->U - s->U1 : -1; }
 
+static nsw_status ensure_flush_buffer(nsw_solver* s) {
+  if (s->flush_buf) return NSW_OK;
+  s->flush_n = size_t(256) << 20;  // 1 GiB of floats > 126 MB L2
+  CUDA_TRY(cudaMalloc((void**)&s->flush_buf, s->flush_n * 4));
+  CUDA_TRY(cudaMemset(s->flush_buf, 0, s->flush_n * 4));
+  return NSW_OK;
+}
+
+// Write 1 GiB (evicts everything from the 126 MB L2), then drop those dirty
+// lines without writing them back: the next step starts from a cold, clean L2
+// instead of paying the flush's own write-backs.
+static nsw_status launch_l2_flush(nsw_solver* s, cudaStream_t st) {
+  flush_kernel<<<sm_count() * 8, 512, 0, st>>>(s->flush_buf, s->flush_n);
+  CUDA_TRY(cudaGetLastError());
+  discard_kernel<<<sm_count() * 8, 512, 0, st>>>(s->flush_buf, s->flush_n);
+  CUDA_TRY(cudaGetLastError());
+  return NSW_OK;
+}
+
+nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream) {
+  if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  nsw_status e = ensure_flush_buffer(s);
+  if (e != NSW_OK) return e;
+  return launch_l2_flush(s, stream ? (cudaStream_t)stream : s->stream);
+}
+
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused) {
   if (!s || steps <= 0) return fail(NSW_ERR_ARG, "bad arguments");
   if (s->world != 1) return fail(NSW_ERR_ARG, "timing helper drives a single shard");
-  if (flush_l2 && !s->flush_buf) {
-    s->flush_n = size_t(256) << 20;  // 1 GiB of floats > 126 MB L2
-    CUDA_TRY(cudaMalloc((void**)&s->flush_buf, s->flush_n * 4));
-    CUDA_TRY(cudaMemset(s->flush_buf, 0, s->flush_n * 4));
+  if (s->tol) return fail(NSW_ERR_ARG, "timing helper runs the fixed schedule");
+  if (flush_l2) {
+    nsw_status fe = ensure_flush_buffer(s);
+    if (fe != NSW_OK) return fe;
   }
+  // One step as the solve runs it, as CUDA graphs: [fused launch(es)] and
+  // [impact reduction + finalize], with events between them so the fused
+  // kernels' share is measured on the same replay.
   std::vector<cudaEvent_t> ev(size_t(3) * steps);
-  for (auto& e : ev) CUDA_TRY(cudaEventCreate(&e));
-  for (int i = 0; i < steps; ++i) {
-    if (flush_l2) {
-      flush_kernel<<<sm_count() * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
-      CUDA_TRY(cudaGetLastError());
-      // drop the flush buffer's dirty lines without writing them back: the
-      // timed step starts from a cold, clean L2 instead of paying the
-      // flush's write-backs
-      discard_kernel<<<sm_count() * 8, 512, 0, s->stream>>>(s->flush_buf, s->flush_n);
-      CUDA_TRY(cudaGetLastError());
+  for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+  const bool fuse = fuse_finalize(s);
+  const int64_t before = s->launches;
+  nsw_status e = NSW_OK;
+  auto capture = [&](cudaGraphExec_t* out, bool fused_part) -> nsw_status {
+    cudaGraph_t g = nullptr;
+    CUDA_TRY(cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal));
+    nsw_status r = NSW_OK;
+    if (fused_part) {
+      r = launch_fused(s, s->stream);
+    } else {
+      r = launch_impact_reduce(s, s->stream, fuse);
+      if (r == NSW_OK && !fuse) r = launch_finalize(s, s->stream);
     }
-    CUDA_TRY(cudaEventRecord(ev[3 * i], s->stream));
-    nsw_status e = launch_fused(s, s->stream);
-    if (e != NSW_OK) return e;
-    CUDA_TRY(cudaEventRecord(ev[3 * i + 1], s->stream));
-    const bool fuse = fuse_finalize(s);
-    e = launch_impact_reduce(s, s->stream, fuse);
-    if (e != NSW_OK) return e;
-    if (!fuse) {
-      finalize_kernel<<<1, 512, 0, s->stream>>>(s->fin);
-      CUDA_TRY(cudaGetLastError());
-      s->launches += 1;
+    cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+    if (r == NSW_OK && ce != cudaSuccess) r = fail(NSW_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    if (r == NSW_OK && cudaGraphInstantiate(out, g, 0) != cudaSuccess) r = fail(NSW_ERR_CUDA, "graph instantiate");
+    if (g) cudaGraphDestroy(g);
+    return r;
+  };
+  cudaGraphExec_t gx = nullptr, gy = nullptr;
+  e = capture(&gx, true);
+  if (e == NSW_OK) e = capture(&gy, false);
+  const int64_t per_step = s->launches - before;
+  s->launches = before;
+  // all steps enqueued ahead (the host never waits inside the timed region)
+  for (int i = 0; i < steps && e == NSW_OK; ++i) {
+    if (flush_l2 && (e = launch_l2_flush(s, s->stream)) != NSW_OK) break;
+    if (cudaEventRecord(ev[3 * i], s->stream) != cudaSuccess || cudaGraphLaunch(gx, s->stream) != cudaSuccess ||
+        cudaEventRecord(ev[3 * i + 1], s->stream) != cudaSuccess || cudaGraphLaunch(gy, s->stream) != cudaSuccess ||
+        cudaEventRecord(ev[3 * i + 2], s->stream) != cudaSuccess) {
+      e = fail(NSW_ERR_CUDA, "timed step failed");
+      break;
     }
-    CUDA_TRY(cudaEventRecord(ev[3 * i + 2], s->stream));
+    s->launches += per_step;
   }
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
+  if (e == NSW_OK && cudaStreamSynchronize(s->stream) != cudaSuccess) e = fail(NSW_ERR_CUDA, "timed steps failed");
   float tot = 0.f, fus = 0.f;
-  for (int i = 0; i < steps; ++i) {
+  for (int i = 0; i < steps && e == NSW_OK; ++i) {
     float a = 0.f, b = 0.f;
-    CUDA_TRY(cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]));
-    CUDA_TRY(cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 1]));
+    cudaEventElapsedTime(&a, ev[3 * i], ev[3 * i + 2]);
+    cudaEventElapsedTime(&b, ev[3 * i], ev[3 * i + 1]);
     tot += a;
     fus += b;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
+  if (gy) cudaGraphExecDestroy(gy);
+  if (gx) cudaGraphExecDestroy(gx);
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (e != NSW_OK) return e;
   if (ms_total) *ms_total = tot;
   if (ms_fused) *ms_fused = fus;
   return NSW_OK;

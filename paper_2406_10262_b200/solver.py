@@ -238,6 +238,10 @@ class DeviceSolver:
     def launch_count(self) -> int:
         return int(self.lib.nsw_solver_launch_count(self.h))
 
+    def flush_l2(self, stream: int | None = None):
+        """Measurement helper: evict the L2 on ``stream`` (1 GiB write + discard)."""
+        check(self.lib.nsw_solver_flush_l2(self.h, C.c_void_p(stream)), "flush_l2")
+
     def time_steps(self, steps: int, flush_l2: bool = True):
         tot, fus = C.c_float(), C.c_float()
         check(self.lib.nsw_solver_time_steps(self.h, int(steps), int(flush_l2), C.byref(tot), C.byref(fus)))
