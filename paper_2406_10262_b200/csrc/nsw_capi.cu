@@ -146,6 +146,8 @@ struct nsw_solver {
   FinalizeArgs fin{};
   float* flush_buf = nullptr;
   size_t flush_n = 0;
+  cudaStream_t side = nullptr;              // tail launch stream (concurrent with the main wave)
+  cudaEvent_t fork = nullptr, join = nullptr;
   unsigned long long* phase_ns = nullptr;  // [U][16] phase stamps (NSW_PHASE_TIMING diagnostics)
 };
 
@@ -265,6 +267,16 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
     s->launches += 1;
     return NSW_OK;
   }
+  // The tail users are independent of the main launch's users within a step:
+  // the tail goes on a side stream forked after the main launch, so its CTAs
+  // start on SMs as soon as the main wave frees them (joined before the
+  // impact reduction).
+  const bool both = s->U1 > 0 && s->U1 < s->U;
+  const bool side = both && s->side != nullptr;
+  if (side) {
+    CUDA_TRY(cudaEventRecord(s->fork, st));
+    CUDA_TRY(cudaStreamWaitEvent(s->side, s->fork, 0));
+  }
   if (s->U1 > 0)
     CUDA_TRY(cudaLaunchKernel(s->var->fn, dim3(s->U1), dim3(s->var->NT), s->dtype == NSW_F64 ? args64 : args32,
                               s->smem, st));
@@ -272,8 +284,12 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
     void* brgs32[] = {&s->b32};
     void* brgs64[] = {&s->b64};
     CUDA_TRY(cudaLaunchKernel(s->var2->fn, dim3(s->U - s->U1), dim3(s->var2->NT),
-                              s->dtype == NSW_F64 ? brgs64 : brgs32, s->smem2, st));
+                              s->dtype == NSW_F64 ? brgs64 : brgs32, s->smem2, side ? s->side : st));
     s->launches += 1;
+  }
+  if (side) {
+    CUDA_TRY(cudaEventRecord(s->join, s->side));
+    CUDA_TRY(cudaStreamWaitEvent(st, s->join, 0));
   }
   s->launches += 1;
   return NSW_OK;
@@ -538,6 +554,15 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     if (s->U1 < users_local) {
       s->var2 = wide;
       s->smem2 = wide->smem(T);
+      const char* tc = std::getenv("NSW_TAIL_CONCURRENT");
+      if (s->U1 > 0 && !(tc && *tc == '0')) {
+        if (cudaStreamCreateWithFlags(&s->side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&s->join, cudaEventDisableTiming) != cudaSuccess) {
+          nsw_solver_destroy(s);
+          return fail(NSW_ERR_CUDA, "side stream creation failed");
+        }
+      }
       if (cudaFuncSetAttribute(wide->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem2)) !=
           cudaSuccess) {
         nsw_solver_destroy(s);
@@ -613,6 +638,9 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
     cudaStreamSynchronize(s->stream);
   }
   if (s->flush_buf) cudaFree(s->flush_buf);
+  if (s->fork) cudaEventDestroy(s->fork);
+  if (s->join) cudaEventDestroy(s->join);
+  if (s->side) cudaStreamDestroy(s->side);
   pinned_state_put(s->state_host);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
