@@ -30,9 +30,11 @@ def top_positions(policy):
     as_torch = isinstance(policy, torch.Tensor)
     x = policy if as_torch else getattr(policy, "values", policy)
     if not as_torch:
-        arr = np.ascontiguousarray(x)
+        arr = np.asarray(x)
         if arr.dtype not in (np.float32, np.float64):
             arr = arr.astype(np.float64)
+        if not arr.flags.writeable or not arr.flags.c_contiguous:
+            arr = np.array(arr, copy=True, order="C")   # torch wants a writable buffer
         x = torch.as_tensor(arr, device="cuda")
     elif x.dtype not in (torch.float32, torch.float64):
         x = x.to(torch.float64)
