@@ -134,3 +134,18 @@ def last_error() -> str:
 def dptr(a):
     """ctypes double* of a C-contiguous float64 ndarray."""
     return a.ctypes.data_as(_dp)
+
+
+def host_to_cuda(x, dtype=None):
+    """numpy-like -> CUDA torch tensor (copies read-only / strided arrays first,
+    which torch cannot wrap); torch tensors pass through (moved/cast if needed)."""
+    import numpy as np
+    import torch
+    if isinstance(x, torch.Tensor):
+        t = x if dtype is None else x.to(dtype)
+        return t.to("cuda").contiguous()
+    a = np.asarray(x)
+    if not a.flags.writeable or not a.flags.c_contiguous:
+        a = np.array(a, copy=True, order="C")
+    t = torch.as_tensor(a, device="cuda")
+    return t if dtype is None else t.to(dtype)

@@ -28,10 +28,7 @@ __all__ = ["user_utility", "mean_max_envy", "items_better_off", "items_worse_off
 
 
 def _dev(x, dtype):
-    import torch
-    if isinstance(x, torch.Tensor):
-        return x.to(device="cuda", dtype=dtype).contiguous()
-    return torch.as_tensor(np.ascontiguousarray(x), dtype=dtype, device="cuda")
+    return _lib.host_to_cuda(x, dtype)
 
 
 def policy_metrics(policy, relevance, exposure, threshold: float = 0.10) -> dict:

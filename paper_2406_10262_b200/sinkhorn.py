@@ -268,7 +268,7 @@ def cost_from_policy(plan, epsilon: float):
     if epsilon <= 0:
         raise DomainError("epsilon must be > 0")
     as_t = isinstance(plan, torch.Tensor)
-    x = plan.contiguous() if as_t else torch.as_tensor(np.ascontiguousarray(plan, dtype=np.float64), device="cuda")
+    x = plan.contiguous() if as_t else _lib.host_to_cuda(np.asarray(plan, dtype=np.float64))
     if x.dtype not in (torch.float32, torch.float64):
         x = x.to(torch.float64)
     out = torch.empty_like(x)
