@@ -277,6 +277,11 @@ nsw_status nsw_cost_from_policy_f64(const double* plan, size_t count, double eps
 nsw_status nsw_cost_from_policy_f32(const float* plan, size_t count, double epsilon, float* cost,
                                     void* stream);
 
+/* Page-locked host memory for results, from a small process-wide cache
+ * (NULL on failure).  Free with nsw_host_free. */
+void* nsw_host_alloc(size_t bytes);
+void nsw_host_free(void* ptr);
+
 /* Whether a (dtype, n, m, iters) problem has a compiled tile variant. */
 int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);
 

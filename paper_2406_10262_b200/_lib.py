@@ -73,6 +73,8 @@ SIGNATURES = {
     "nsw_solver_top_positions": (C.c_int, [_vp, C.POINTER(_i32)]),
     "nsw_solver_metrics": (C.c_int, [_vp, C.c_double, _dp]),
     "nsw_solver_flush_l2": (C.c_int, [_vp, _vp]),
+    "nsw_host_alloc": (_vp, [C.c_size_t]),
+    "nsw_host_free": (None, [_vp]),
     "nsw_solver_bind_tol_exchange": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_local": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_decide": (C.c_int, [_vp, _vp, C.POINTER(_i32)]),

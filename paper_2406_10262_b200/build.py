@@ -86,7 +86,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
         tmp = LIB + ".tmp"
-        cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lcublas"]
+        cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr}")

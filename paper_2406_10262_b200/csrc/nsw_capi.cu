@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -391,6 +392,14 @@ void pinned_state_put(int* p) {
   g_pinned_free.push_back(p);
 }
 
+// Page-locked host blocks for results (the policy tensor): a small
+// process-wide cache keyed by size, so repeated solves neither pay
+// cudaHostAlloc nor fault fresh pageable memory.
+std::mutex g_host_mu;
+std::multimap<size_t, void*> g_host_free;
+std::map<void*, size_t> g_host_size;
+constexpr size_t kHostCacheBlocks = 8;
+
 nsw_status keep_pool_memory(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return NSW_OK;
@@ -407,6 +416,37 @@ nsw_status keep_pool_memory(int device) {
 extern "C" {
 
 const char* nsw_last_error(void) { return g_err.c_str(); }
+void* nsw_host_alloc(size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_free.find(bytes);
+    if (it != g_host_free.end()) {
+      void* p = it->second;
+      g_host_free.erase(it);
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  g_host_size[p] = bytes;
+  return p;
+}
+
+void nsw_host_free(void* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  auto it = g_host_size.find(p);
+  if (it == g_host_size.end()) return;
+  if (g_host_free.size() < kHostCacheBlocks) {
+    g_host_free.emplace(it->second, p);
+    return;
+  }
+  g_host_size.erase(it);
+  cudaFreeHost(p);
+}
+
 const char* nsw_version(void) { return "nswrank_b200 0.1.0 (sm_100a)"; }
 
 int32_t nsw_supported(int32_t dtype, int32_t n, int32_t m, int32_t iters) {

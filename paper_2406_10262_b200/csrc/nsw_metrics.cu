@@ -9,6 +9,7 @@
 // allocation masses, impacts and row maxima are kernels here.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -117,12 +118,40 @@ __global__ void metrics_finish_kernel(const double* __restrict__ imp, const doub
   }
 }
 
+// cuBLAS is loaded on first use (dlopen), so the solver library does not pull
+// it in at import time; only the envy product of the metrics needs it.
+struct Cublas {
+  using create_t = cublasStatus_t (*)(cublasHandle_t*);
+  using stream_t = cublasStatus_t (*)(cublasHandle_t, cudaStream_t);
+  using dgemm_t = cublasStatus_t (*)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
+                                     const double*, const double*, int, const double*, int, const double*, double*,
+                                     int);
+  create_t create = nullptr;
+  stream_t set_stream = nullptr;
+  dgemm_t dgemm = nullptr;
+  bool ok = false;
+  Cublas() {
+    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_LOCAL);
+    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    create = reinterpret_cast<create_t>(dlsym(h, "cublasCreate_v2"));
+    set_stream = reinterpret_cast<stream_t>(dlsym(h, "cublasSetStream_v2"));
+    dgemm = reinterpret_cast<dgemm_t>(dlsym(h, "cublasDgemm_v2"));
+    ok = create && set_stream && dgemm;
+  }
+};
+
+const Cublas& cublas() {
+  static const Cublas c;
+  return c;
+}
+
 // one cuBLAS handle per host thread and device (creating one costs ms)
 cublasHandle_t cublas_handle() {
   thread_local cublasHandle_t handles[64] = {};
   int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!handles[dev] && cublasCreate(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
+  if (!cublas().ok || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!handles[dev] && cublas().create(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
   return handles[dev];
 }
 
@@ -178,9 +207,9 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
       else widen_to_f64<<<sm_count() * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
     }
     if (status == NSW_OK && (h = cublas_handle()) == nullptr) status = NSW_ERR_CUDA;
-    if (status == NSW_OK && cublasSetStream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
-    if (status == NSW_OK &&
-        cublasDgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, U, &one, Rd, n, A, n, &zero, cross, n) != CUBLAS_STATUS_SUCCESS)
+    if (status == NSW_OK && cublas().set_stream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
+    if (status == NSW_OK && cublas().dgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, U, &one, Rd, n, A, n, &zero, cross,
+                                           n) != CUBLAS_STATUS_SUCCESS)
       status = NSW_ERR_CUDA;
     if (status == NSW_OK) {
       envy_kernel<<<(n + 127) / 128, 128, 0, st>>>(cross, n, envy);

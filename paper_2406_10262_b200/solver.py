@@ -312,17 +312,32 @@ class DeviceSolver:
         return pol, trace
 
 
+class _HostBlock:
+    """Owner of a page-locked block from the library's host cache; freed
+    (returned to the cache) when the last array viewing it goes away."""
+
+    def __init__(self, lib, ptr):
+        self.lib, self.ptr = lib, ptr
+
+    def __del__(self):
+        try:
+            self.lib.nsw_host_free(self.ptr)
+        except Exception:
+            pass
+
+
 def _host_buffer(shape) -> np.ndarray:
-    """float64 host array for a device result: page-locked through torch's
-    caching host allocator when torch is present (the copy runs at full link
-    speed and repeated solves reuse the block), else pageable."""
-    try:
-        import torch
-        if torch.cuda.is_available():
-            return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
-    except Exception:
-        pass
-    return np.empty(shape, dtype=np.float64)
+    """float64 host array for a device result, page-locked (the copy runs at
+    full link speed and repeated solves reuse the block); pageable if the
+    allocation fails."""
+    count = int(np.prod(shape))
+    lib = _lib.load()
+    ptr = lib.nsw_host_alloc(count * 8)
+    if not ptr:
+        return np.empty(shape, dtype=np.float64)
+    buf = (C.c_double * count).from_address(ptr)
+    buf._owner = _HostBlock(lib, ptr)
+    return np.ctypeslib.as_array(buf).reshape(shape)
 
 
 def solve_fair_ranking(relevance, exposure, shape, config, options: DeviceOptions | None = None):
