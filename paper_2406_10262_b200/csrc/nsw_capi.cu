@@ -574,6 +574,31 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   if (options->variant == -1 && var->CL == 1) {
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
+    // Fewer users than one wave of the throughput tile (e.g. a strong-scaling
+    // shard): the tile with the fewest rows per thread (R >= 2) that still
+    // holds every user in one wave has the shortest per-user latency
+    // (config 1 at 149..444 users per GPU: R=4/NT=128 is 28 % faster than
+    // R=8/NT=64).  At most one user per SM goes to the wide tile below.
+    if (!std::getenv("NSW_MAIN_TILE") && users_local > sms) {
+      const Variant* low = nullptr;
+      for (auto& v : variant_registry()) {
+        if (v.dtype != var->dtype || v.M != var->M || v.CL != 1 || v.rows < n || v.R < 2 ||
+            v.smem(T) > kMaxSmem || v.R >= var->R)
+          continue;
+        int ps = 0;
+        if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v.smem(T))) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, v.fn, v.NT, v.smem(T)) != cudaSuccess)
+          continue;
+        if (ps * sms >= users_local &&
+            (!low || v.R < low->R || (v.R == low->R && (v.NT < low->NT || (v.NT == low->NT && v.minb < low->minb)))))
+          low = &v;
+      }
+      if (low) {
+        var = low;
+        s->var = low;
+        s->smem = low->smem(T);
+      }
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);
     const Variant* wide = choose_wide_variant(var, n, T);
     if (const char* e = std::getenv("NSW_TAIL_TILE")) {   // experiments: "R,NT" of the tail tile

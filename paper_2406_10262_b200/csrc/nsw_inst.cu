@@ -67,6 +67,7 @@ NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)
 NSW_REG(8, 64, 6)
 NSW_REG(4, 128, 3)
+NSW_REG(4, 128, 4)   // 4 per SM: one wave of up to 592 users (strong-scaling shards)
 NSW_REG(8, 128, 3)
 NSW_REG(8, 256, 1)
 NSW_REG(2, 256, 1)

@@ -21,6 +21,7 @@ def main():
     solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(4, 50, 11),
                        SolverConfig(outer_max_iters=2), DeviceOptions())
     print(f"first solve (module loading) {time.perf_counter() - t0:.2f} s")
+    chunk = int(os.environ.get("TOL_CHUNK", "16"))
     for name, users, eps, dtype in (("cfg0", 100, 0.1, "float64"), ("cfg1", 1000, 0.05, "float64"),
                                     ("cfg1", 1000, 0.05, "float32")):
         rel, expo, _ = make_instance(name, seed=0, num_users=users)
@@ -29,12 +30,12 @@ def main():
         args = (RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, expo.size + 1), cfg)
         t0 = time.perf_counter()
         try:
-            pol, tr = solve_fair_ranking(*args, DeviceOptions(dtype=dtype, schedule="tolerance"))
+            pol, tr = solve_fair_ranking(*args, DeviceOptions(dtype=dtype, schedule="tolerance", tol_chunk=chunk))
         except SolverError as e:
             tr = e.trace
         dt = time.perf_counter() - t0
         its = tr.sinkhorn_iterations
-        print(f"{name} U={U} {dtype}: {len(tr)} steps in {dt*1e3:.1f} ms ({dt/len(tr)*1e3:.2f} ms/step), "
+        print(f"chunk {chunk} {name} U={U} {dtype}: {len(tr)} steps in {dt*1e3:.1f} ms ({dt/len(tr)*1e3:.2f} ms/step), "
               f"inner iterations {its[:3]}..{its[-3:]} total {sum(its)}, "
               f"{sum(its)/dt:.0f} inner it/s")
 
