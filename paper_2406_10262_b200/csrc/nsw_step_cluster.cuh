@@ -33,7 +33,33 @@ template <typename S, int MC, int CG, int R, int NT, int CL>
 __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
   return sizeof(S) * (size_t(Tl::NR) * Tl::P + size_t(T + 1) * Tl::P + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
-                      2 * size_t(Tl::NR) + 2 * Tl::P + 4);
+                      2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P) +
+         32;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned)
+}
+
+// DSMEM push exchange of the per-CTA column totals: every CTA stores its
+// totals into slot [parity][its rank] of every CTA of the cluster with
+// st.async, which completes bytes on the receiver's mbarrier; a receiver
+// waits on its own mbarrier (no cluster-wide barrier per reduction).
+__device__ __forceinline__ uint32_t cl_map(uint32_t local_saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st_async(uint32_t raddr, float v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(raddr),
+               "r"(__float_as_uint(v)), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st_async(uint32_t raddr, double v, uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_expect_tx(uint32_t mbar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(mbar),
+               "r"(bytes)
+               : "memory");
 }
 
 // Reduce-scatter across the row-group lanes (xor offsets 16 .. CG).
@@ -117,11 +143,22 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   S* rowA = vec2 + P;                       // [NR]
   S* rowB = rowA + NR;                      // [NR]
   S* clred = rowB + NR;                     // [2][P] this CTA's column totals
+  S* xch = clred + 2 * P;                   // [2][CL][P] exchange slots (pushed by every rank)
+  uint64_t* xmb = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(xch + 2 * CL * P) + 7) & ~uintptr_t(7));
 
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) {
     cluster.sync();
     return;
+  }
+  uint32_t xph = 0;   // mbarrier phase bit per exchange buffer
+  if constexpr (CL > 1) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(xmb)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(xmb + 1)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cluster.sync();   // every CTA's mbarriers exist before anyone pushes
   }
   const int rank = int(cluster.block_rank());
   const int u = a.user0 + int(blockIdx.x) / CL;
@@ -169,16 +206,21 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       acc = red[tid];
 #pragma unroll
       for (int w = 1; w < NW; ++w) acc += red[w * P + tid];
-      if constexpr (CL > 1) clred[parity * P + tid] = acc;
     }
     if constexpr (CL > 1) {
-      cluster.sync();
+      const uint32_t mb = smem_u32(xmb + parity);
+      if (tid == 0) cl_expect_tx(mb, uint32_t(CL * m * sizeof(S)));
       if (tid < m) {
+        const uint32_t slot = smem_u32(xch + (size_t(parity) * CL + rank) * P + tid);
+#pragma unroll
+        for (int q = 0; q < CL; ++q) cl_st_async(cl_map(slot, q), acc, cl_map(mb, q));
+        mbar_wait(mb, (xph >> parity) & 1u);
         S tot = S(0);
 #pragma unroll
-        for (int q = 0; q < CL; ++q) tot += *cluster.map_shared_rank(clred + parity * P + tid, q);
+        for (int q = 0; q < CL; ++q) tot += xch[(size_t(parity) * CL + q) * P + tid];   // rank order
         fin(tid, tot);
       }
+      xph ^= 1u << parity;
       parity ^= 1;
     } else {
       if (tid < m) fin(tid, acc);
