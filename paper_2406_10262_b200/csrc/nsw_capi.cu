@@ -567,10 +567,6 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   // Wave split: whole waves of the main tile, then (if what is left is at
   // most one user per SM) a tail launch with the wide tile.
   s->U1 = users_local;
-  if (var->CL > 1 && options->schedule == NSW_SCHEDULE_TOLERANCE) {
-    nsw_solver_destroy(s);
-    return fail(NSW_ERR_UNSUPPORTED, "tolerance schedule is not available for cluster tiles (m > 32 or large n)");
-  }
   if (options->variant == -1 && var->CL == 1) {
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);

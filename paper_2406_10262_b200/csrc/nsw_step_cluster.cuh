@@ -33,8 +33,8 @@ template <typename S, int MC, int CG, int R, int NT, int CL>
 __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
   return sizeof(S) * (size_t(Tl::NR) * Tl::P + size_t(T + 1) * Tl::P + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
-                      2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P) +
-         32;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned)
+                      2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P + 2 * Tl::P + Tl::NW) +
+         48;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned) + residual scratch
 }
 
 // DSMEM push exchange of the per-CTA column totals: every CTA stores its
@@ -145,6 +145,8 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   S* clred = rowB + NR;                     // [2][P] this CTA's column totals
   S* xch = clred + 2 * P;                   // [2][CL][P] exchange slots (pushed by every rank)
   uint64_t* xmb = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(xch + 2 * CL * P) + 7) & ~uintptr_t(7));
+  S* colres = reinterpret_cast<S*>(xmb + 2);   // [2][P] column residuals (tolerance mode)
+  S* rmw = colres + 2 * P;                      // [NW] per-warp row-residual maxima
 
   const int phase = a.state[ST_PHASE];
   if (phase == PHASE_FINISHED) {
@@ -160,6 +162,10 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
     cluster.sync();   // every CTA's mbarriers exist before anyone pushes
   }
+  const bool tolm = a.tol_mode != 0;
+  // length of the v~ history of the K~ this launch rebuilds (see step_kernel)
+  const int Tprev = tolm ? a.state[ST_TSTAR] : T;
+  const int Th = phase == PHASE_FWD_CONT ? a.state[ST_T0] : (phase == PHASE_FWD_FIN ? a.state[ST_TSTAR] : Tprev);
   const int rank = int(cluster.block_rank());
   const int u = a.user0 + int(blockIdx.x) / CL;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -191,7 +197,9 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   };
   // column reduction over the whole cluster; fin(k, total) on thread k < m
   // of every CTA (identical bits everywhere)
-  auto reduce_cols = [&](S (&v)[MC], auto&& fin) {
+  // xval: this CTA's row-residual max (tolerance mode) travels in slot m of
+  // the exchange; the cluster maximum is returned in *xmax on thread m
+  auto reduce_cols = [&](S (&v)[MC], auto&& fin, bool xon = false, S xval = S(0), S* xmax = nullptr) {
     int base = 0, lim = MC;
     rs_rows<S, MC, MC, 16, CG, OpSum>(v, lane, base, lim);
     constexpr int CF = rs_final_count<MC, 16, CG>();
@@ -209,21 +217,31 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
     if constexpr (CL > 1) {
       const uint32_t mb = smem_u32(xmb + parity);
-      if (tid == 0) cl_expect_tx(mb, uint32_t(CL * m * sizeof(S)));
-      if (tid < m) {
+      const int nx = m + (xon ? 1 : 0);
+      if (tid == 0) cl_expect_tx(mb, uint32_t(CL * nx * sizeof(S)));
+      if (tid < nx) {
+        const S mine = tid < m ? acc : xval;
         const uint32_t slot = smem_u32(xch + (size_t(parity) * CL + rank) * P + tid);
 #pragma unroll
-        for (int q = 0; q < CL; ++q) cl_st_async(cl_map(slot, q), acc, cl_map(mb, q));
+        for (int q = 0; q < CL; ++q) cl_st_async(cl_map(slot, q), mine, cl_map(mb, q));
         mbar_wait(mb, (xph >> parity) & 1u);
-        S tot = S(0);
+        if (tid < m) {
+          S tot = S(0);
 #pragma unroll
-        for (int q = 0; q < CL; ++q) tot += xch[(size_t(parity) * CL + q) * P + tid];   // rank order
-        fin(tid, tot);
+          for (int q = 0; q < CL; ++q) tot += xch[(size_t(parity) * CL + q) * P + tid];   // rank order
+          fin(tid, tot);
+        } else {
+          S mx = S(0);
+#pragma unroll
+          for (int q = 0; q < CL; ++q) mx = fmax(mx, xch[(size_t(parity) * CL + q) * P + tid]);
+          *xmax = mx;
+        }
       }
       xph ^= 1u << parity;
       parity ^= 1;
     } else {
       if (tid < m) fin(tid, acc);
+      if (xon && tid == m) *xmax = xval;
     }
     __syncthreads();
   };
@@ -249,11 +267,12 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   for (int j = 0; j < MC; ++j) ex[j] = (col(j) < m - 1) ? a.expo[min(col(j), m - 2)] : S(0);
   __syncthreads();
 
-  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING) {
-    // ---- rebuild K~ of step k-1 (this CTA's items) ----
+  if (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING || phase == PHASE_FWD_CONT || phase == PHASE_FWD_FIN) {
+    // ---- rebuild K~ (step k-1's for the backward; this step's for a
+    // tolerance-mode continuation / finish) of this CTA's items ----
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
     for (int i = tid; i < nloc; i += NT) rowA[i] = a.alpha[size_t(u) * n + r0 + i];
-    for (int idx = tid; idx < (T + 1) * P; idx += NT) {
+    for (int idx = tid; idx < (Th + 1) * P; idx += NT) {
       const int t = idx / P, k = idx - t * P;
       vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
     }
@@ -275,11 +294,11 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     __syncthreads();
     S vT[MC];
 #pragma unroll
-    for (int j = 0; j < MC; ++j) vT[j] = vh[size_t(T) * P + col(j)];
+    for (int j = 0; j < MC; ++j) vT[j] = vh[size_t(Th) * P + col(j)];
     {
       S vT1[MC];
 #pragma unroll
-      for (int j = 0; j < MC; ++j) vT1[j] = vh[size_t(T - 1) * P + col(j)];
+      for (int j = 0; j < MC; ++j) vT1[j] = vh[size_t(Th - 1) * P + col(j)];
       for (int r = 0; r < R; ++r) {   // u~^T (all lanes of the group agree)
         S kr[MC];
         ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * P + g * MC);
@@ -297,12 +316,12 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
           V16<S> t;
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(Th) * P + k]);
             if (++k == m) { k = 0; ++i; }
           }
           reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
         } else {
-          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(T) * P + k]);
+          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(Th) * P + k]);
         }
       });
     };
@@ -310,6 +329,31 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       if (improved) write_policy();
       cluster.sync();
       return;
+    }
+    if (phase == PHASE_FWD_FIN) {
+      // tolerance mode: the forward stopped at t* = Th; impact terms of X^{t*}
+#pragma unroll 1
+      for (int r = 0; r < R; ++r) {
+        const int il = lrow(r);
+        S kr[MC];
+        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        const double rr = ok(r) ? double(relu[il]) : 0.0;
+        const S uT = rowA[il];
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < MC; ++j)
+          if (col(j) < m - 1) acc = fma(rr * a.expo_d[min(col(j), m - 2)], double(mul_(mul_(kr[j], uT), vT[j])), acc);
+        acc = group_sum<double, CG>(acc);
+        if (g == 0 && ok(r)) a.partial[size_t(u) * n + r0 + il] = acc;
+      }
+      cluster.sync();
+      return;
+    }
+    if (phase == PHASE_FWD_CONT) {
+      // tolerance mode: continue this step's forward from v~^{t0}, t0 = Th
+      if (tid < P) vec0[tid] = vh[size_t(Th) * P + tid];
+      __syncthreads();
+      goto forward_iterations;
     }
     if (improved) write_policy();
 
@@ -342,9 +386,9 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         gsum = group_sum<S, CG>(gsum);
         if (g == 0) rowB[il] = gsum;
       }
-      reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vh[size_t(T) * P + k], tot), inv_mass(k)); });
+      reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k)); });
     }
-    for (int t = T; t >= 1; --t) {
+    for (int t = Th; t >= 1; --t) {
       S cv[MC], vp[MC], vpp[MC], c[MC];
 #pragma unroll
       for (int j = 0; j < MC; ++j) {
@@ -353,7 +397,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         vpp[j] = vh[size_t(t >= 2 ? t - 2 : 0) * P + col(j)];
         c[j] = S(0);
       }
-      const bool first = t == T;
+      const bool first = t == Th;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
@@ -395,7 +439,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       }
       st_seg<S, MC>(Kt + size_t(il) * P + g * MC, gk);
     }
-    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(T) * P + tid])) : S(0);
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
     __syncthreads();
     // ---- Adam ascent on this CTA's cells ----
     const int s = a.state[ST_STEP];
@@ -490,6 +534,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
   }
   __syncthreads();
+forward_iterations:
   S A[R][MC];
   S ut[R];
 #pragma unroll
@@ -497,13 +542,31 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     ld_seg<S, MC>(A[r], Kt + size_t(lrow(r)) * P + g * MC);
     ut[r] = S(0);
   }
-  for (int t = 1; t <= T; ++t) {
+  const int t_start = phase == PHASE_FWD_CONT ? Th + 1 : 1;
+  const int t_end = tolm ? min(t_start - 1 + a.chunk, T) : T;
+  // tolerance mode also records the reference's L-inf marginal residual of
+  // every iteration (sinkhorn.py:237-243), as step_kernel does: the row
+  // residual of iteration t-1 from iteration t's own row dot (max over the
+  // cluster through the exchange), the column residual (fp64) in fin
+  auto row_res_max = [&](S rm) -> S {   // CTA maximum, valid on every thread after the barrier
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) rm = fmax(rm, __shfl_xor_sync(0xffffffffu, rm, o));
+    if (lane == 0) rmw[warp] = rm;
+    __syncthreads();
+    S r = S(0);
+    for (int w = 0; w < NW; ++w) r = fmax(r, rmw[w]);
+    return r;
+  };
+  for (int t = t_start; t <= t_end; ++t) {
     S vv[MC], c[MC];
 #pragma unroll
     for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+    S rmax = S(0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const S rp = F::rcp_fast(rdot_g<S, MC, CG>(A[r], vv));
+      const S sr = rdot_g<S, MC, CG>(A[r], vv);
+      if (tolm && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
+      const S rp = F::rcp_fast(sr);
       ut[r] = ok(r) ? rp : S(0);
     }
 #pragma unroll
@@ -512,11 +575,47 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
 #pragma unroll
       for (int r = 1; r < R; ++r) c[j] = fma(A[r][j], ut[r], c[j]);
     }
-    reduce_cols(c, [&](int k, S tot) {
-      const S vn = F::div_fast(mass(k), tot);
-      vec0[k] = vn;
-      if (rank == 0) hu[size_t(t) * m + k] = vn;
-    });
+    const bool rec = tolm && t > t_start;   // residual of iteration t-1 completes here
+    S rcta = S(0), rall = S(0);
+    if (rec) rcta = row_res_max(rmax);
+    reduce_cols(
+        c,
+        [&](int k, S tot) {
+          const S vn = F::div_fast(mass(k), tot);
+          vec0[k] = vn;
+          if (rank == 0) hu[size_t(t) * m + k] = vn;
+          if (tolm) colres[(t & 1) * P + k] = sizeof(S) == 8 ? S(fabs(vn * tot - mass(k))) : S(0);
+        },
+        rec, rcta, &rall);
+    if (rec && rank == 0 && tid == m) {
+      S r = rall;
+      for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[((t - 1) & 1) * P + kk]);
+      a.res[size_t(u) * (T + 1) + t - 1] = double(r);
+    }
+  }
+  if (tolm) {
+    // residual of the chunk's last iteration: one more row pass; cluster max
+    // through distributed shared memory (once per chunk)
+    S vv[MC];
+#pragma unroll
+    for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+    S rmax = S(0);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const S sr = rdot_g<S, MC, CG>(A[r], vv);
+      if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
+    }
+    const S rcta = row_res_max(rmax);
+    if (tid == 0) clred[0] = rcta;
+    cluster.sync();
+    if (rank == 0 && tid == 0) {
+      S r = S(0);
+      for (int q = 0; q < CL; ++q) r = fmax(r, *cluster.map_shared_rank(clred, q));
+      for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[(t_end & 1) * P + kk]);
+      a.res[size_t(u) * (T + 1) + t_end] = double(r);
+    }
+    cluster.sync();   // remote reads done before any CTA exits
+    return;           // impact terms come from the finish launch once t* is known
   }
   // per-item impact terms, float64, completed across the group
   {

@@ -69,3 +69,42 @@ def test_cfg4_shape_fp32_one_step():
     # fp32 at eps=0.01 (|K| ~ 1e2) and Adam's lr/eps gain on gradients below
     # fp32 resolution bound one-step C parity (SURVEY findings 4, P8, P15)
     assert dx <= 1e-5 and (dcell > 1e-3).sum() == 0
+
+
+@pytest.mark.parametrize("U,n,m,eps,chunk", [
+    (4, 300, 40, 0.3, 2),     # 4-CTA cluster (fp64 tile: 128 items per CTA), many continuations
+    (3, 700, 51, 0.3, 3),     # 8-CTA cluster, chunks not dividing the iteration counts
+    (2, 100, 33, 0.4, 16),    # single-CTA cluster tile, one chunk
+])
+def test_cluster_tolerance_schedule_vs_oracle(U, n, m, eps, chunk):
+    """The reference's default stopping rule on cluster tiles: the residual of
+    every iteration is measured across the cluster's CTAs; the lock-step stop,
+    the inner-iteration counts and the policy follow the oracle."""
+    rng = np.random.default_rng(n * 3 + m)
+    rel = np.clip(rng.uniform(0.05, 1.0, (U, n)), 1e-6, 1.0)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    p = orc.SolverParams(epsilon=eps, sinkhorn_max_iters=150, sinkhorn_tol=1e-6, outer_max_iters=6,
+                         grad_threshold=1e-300, fixed_schedule=False)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    cfg = SolverConfig(epsilon=eps, sinkhorn_max_iters=150, sinkhorn_tol=1e-6, outer_max_iters=6,
+                       grad_threshold=1e-300)
+    pol, trd = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg,
+                                  DeviceOptions(dtype="float64", schedule="tolerance", tol_chunk=chunk))
+    print(f"cluster tolerance n={n} m={m}: iterations {trd.sinkhorn_iterations} vs {tro.sinkhorn_iterations}")
+    assert trd.sinkhorn_iterations == tro.sinkhorn_iterations
+    assert len(set(tro.sinkhorn_iterations)) > 1
+    assert max(tro.sinkhorn_iterations) > chunk or chunk == 16
+    assert np.abs(pol.values - xo).max() <= 1e-9
+
+
+def test_cluster_tolerance_fp32_runs():
+    rng = np.random.default_rng(5)
+    U, n, m = 3, 2000, 51
+    rel = np.clip(rng.uniform(0.05, 1.0, (U, n)), 1e-6, 1.0).astype(np.float32).astype(np.float64)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    cfg = SolverConfig(epsilon=0.3, sinkhorn_max_iters=200, sinkhorn_tol=1e-5, outer_max_iters=4,
+                       grad_threshold=1e-300)
+    pol, tr = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg,
+                                 DeviceOptions(dtype="float32", schedule="tolerance"))
+    assert np.isfinite(pol.values).all() and len(tr) == 4
+    assert all(1 <= t <= 200 for t in tr.sinkhorn_iterations)
