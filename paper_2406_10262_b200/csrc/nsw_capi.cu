@@ -560,6 +560,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaMallocHost failed");
   }
+  if (var->CL > 8 && cudaFuncSetAttribute(var->fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+    nsw_solver_destroy(s);
+    return fail(NSW_ERR_UNSUPPORTED, "16-CTA clusters are not available on this device");
+  }
   if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) != cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");

@@ -32,6 +32,7 @@ NSW_REG_CL(1)
 NSW_REG_CL(2)
 NSW_REG_CL(4)
 NSW_REG_CL(8)
+NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8192 (fp32) / 2048 (fp64)
 
 }  // namespace
 }  // namespace nsw

@@ -39,7 +39,9 @@ def test_library_is_sm100a_only():
 
 
 @pytest.mark.parametrize("dtype,n,m,T", [(0, 500, 11, 100), (0, 1000, 21, 100), (0, 2000, 11, 50),
-                                          (1, 50, 11, 50), (1, 500, 11, 100), (0, 7, 4, 9), (1, 65, 30, 6)])
+                                          (1, 50, 11, 50), (1, 500, 11, 100), (0, 7, 4, 9), (1, 65, 30, 6),
+                                          (0, 4000, 51, 200), (0, 8000, 51, 20), (1, 2000, 51, 20),
+                                          (1, 2048, 11, 100)])
 def test_supported_variants(dtype, n, m, T):
     assert _lib.load().nsw_supported(dtype, n, m, T) == 1
 
@@ -47,6 +49,8 @@ def test_supported_variants(dtype, n, m, T):
 def test_unsupported_shapes_reported():
     lib = _lib.load()
     assert lib.nsw_supported(0, 100, 60, 10) == 0    # m > 52: no tile yet
+    assert lib.nsw_supported(0, 9000, 11, 10) == 0   # n > 8192 (16 CTAs x 512 items)
+    assert lib.nsw_supported(1, 4000, 11, 10) == 0   # float64 beyond 2048 items
 
 
 def _create(rel, expo, n, m, cfg, opt):

@@ -108,3 +108,35 @@ def test_cluster_tolerance_fp32_runs():
                                  DeviceOptions(dtype="float32", schedule="tolerance"))
     assert np.isfinite(pol.values).all() and len(tr) == 4
     assert all(1 <= t <= 200 for t in tr.sinkhorn_iterations)
+
+
+def test_cluster16_fp64_vs_oracle():
+    """16-CTA clusters (non-portable size): float64 with 1500 items x 20
+    positions (beyond the 1-CTA float64 tiles and 8-CTA clusters)."""
+    rng = np.random.default_rng(16)
+    U, n, m = 2, 1500, 20
+    rel = np.clip(rng.uniform(0.0, 1.0, (U, n)), 1e-6, 1.0)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    p = orc.SolverParams(epsilon=0.1, sinkhorn_max_iters=8, outer_max_iters=3, grad_threshold=1e-300)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    xd, trd = _solve(rel, expo, 0.1, 8, 3, F64)
+    assert np.abs(xd - xo).max() <= 1e-9
+    assert np.abs(np.array(trd.objective) / np.array(tro.objective) - 1).max() <= 1e-12
+
+
+def test_cluster16_fp32_large_n():
+    """float32 with 6000 items: a 16-CTA cluster of 512-item CTAs."""
+    from paper_2406_10262_b200 import DeviceSolver
+    rng = np.random.default_rng(17)
+    U, n, m = 2, 6000, 11
+    rel = np.clip(rng.uniform(0.0, 1.0, (U, n)), 1e-6, 1.0).astype(np.float32).astype(np.float64)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    cfg = SolverConfig(epsilon=0.1, sinkhorn_max_iters=6, outer_max_iters=3, grad_threshold=1e-300)
+    with DeviceSolver(rel, expo, n, m, cfg, F32) as s:
+        assert s.variant()["NT"] == 256
+        s.run(4)
+        xd, trd = s.result()
+    p = orc.SolverParams(epsilon=0.1, sinkhorn_max_iters=6, outer_max_iters=3, grad_threshold=1e-300)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    assert np.abs(xd - xo).max() <= 1e-4
+    assert np.abs(np.array(trd.objective) / np.array(tro.objective) - 1).max() <= 1e-6
