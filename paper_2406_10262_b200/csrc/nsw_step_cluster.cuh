@@ -557,41 +557,59 @@ forward_iterations:
     for (int w = 0; w < NW; ++w) r = fmax(r, rmw[w]);
     return r;
   };
-  for (int t = t_start; t <= t_end; ++t) {
-    S vv[MC], c[MC];
+  // the iteration body is instantiated twice so the fixed schedule carries
+  // no residual bookkeeping at all
+  auto iterate = [&](auto tol_c) {
+    constexpr bool TOLM = decltype(tol_c)::value;
+    for (int t = t_start; t <= t_end; ++t) {
+      S vv[MC], c[MC];
 #pragma unroll
-    for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
-    S rmax = S(0);
+      for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+      S rmax = S(0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const S sr = rdot_g<S, MC, CG>(A[r], vv);
-      if (tolm && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
-      const S rp = F::rcp_fast(sr);
-      ut[r] = ok(r) ? rp : S(0);
-    }
+      for (int r = 0; r < R; ++r) {
+        const S sr = rdot_g<S, MC, CG>(A[r], vv);
+        if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
+        const S rp = F::rcp_fast(sr);
+        ut[r] = ok(r) ? rp : S(0);
+      }
 #pragma unroll
-    for (int j = 0; j < MC; ++j) {
-      c[j] = A[0][j] * ut[0];
+      for (int j = 0; j < MC; ++j) {
+        c[j] = A[0][j] * ut[0];
 #pragma unroll
-      for (int r = 1; r < R; ++r) c[j] = fma(A[r][j], ut[r], c[j]);
-    }
-    const bool rec = tolm && t > t_start;   // residual of iteration t-1 completes here
-    S rcta = S(0), rall = S(0);
-    if (rec) rcta = row_res_max(rmax);
-    reduce_cols(
-        c,
-        [&](int k, S tot) {
+        for (int r = 1; r < R; ++r) c[j] = fma(A[r][j], ut[r], c[j]);
+      }
+      if constexpr (TOLM) {
+        const bool rec = t > t_start;   // residual of iteration t-1 completes here
+        S rcta = S(0), rall = S(0);
+        if (rec) rcta = row_res_max(rmax);
+        reduce_cols(
+            c,
+            [&](int k, S tot) {
+              const S vn = F::div_fast(mass(k), tot);
+              vec0[k] = vn;
+              if (rank == 0) hu[size_t(t) * m + k] = vn;
+              colres[(t & 1) * P + k] = sizeof(S) == 8 ? S(fabs(vn * tot - mass(k))) : S(0);
+            },
+            rec, rcta, &rall);
+        if (rec && rank == 0 && tid == m) {
+          S r = rall;
+          for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[((t - 1) & 1) * P + kk]);
+          a.res[size_t(u) * (T + 1) + t - 1] = double(r);
+        }
+      } else {
+        reduce_cols(c, [&](int k, S tot) {
           const S vn = F::div_fast(mass(k), tot);
           vec0[k] = vn;
           if (rank == 0) hu[size_t(t) * m + k] = vn;
-          if (tolm) colres[(t & 1) * P + k] = sizeof(S) == 8 ? S(fabs(vn * tot - mass(k))) : S(0);
-        },
-        rec, rcta, &rall);
-    if (rec && rank == 0 && tid == m) {
-      S r = rall;
-      for (int kk = 0; kk < m; ++kk) r = fmax(r, colres[((t - 1) & 1) * P + kk]);
-      a.res[size_t(u) * (T + 1) + t - 1] = double(r);
+        });
+      }
     }
+  };
+  if (tolm) {
+    iterate(std::true_type{});
+  } else {
+    iterate(std::false_type{});
   }
   if (tolm) {
     // residual of the chunk's last iteration: one more row pass; cluster max
