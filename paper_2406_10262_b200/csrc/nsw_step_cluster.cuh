@@ -32,7 +32,8 @@ struct ClTile {
 template <typename S, int MC, int CG, int R, int NT, int CL>
 __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
-  return sizeof(S) * (size_t(Tl::NR) * Tl::P + size_t(T + 1) * Tl::P + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
+  (void)T;   // the v~ history is streamed through a 4-row ring: shared memory does not grow with T
+  return sizeof(S) * (size_t(Tl::NR) * Tl::P + 5 * size_t(Tl::P) + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
                       2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P + 2 * Tl::P + Tl::NW) +
          48;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned) + residual scratch
 }
@@ -135,8 +136,9 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][P]
-  S* vh = Kt + size_t(NR) * P;              // [T+1][P]
-  S* red = vh + size_t(T + 1) * P;          // [NW][P]
+  S* vr = Kt + size_t(NR) * P;              // [4][P] ring of v~ history rows (row t in slot t & 3)
+  S* vTr = vr + 4 * P;                      // [P] row Th of the history (v~ of the solve being differentiated)
+  S* red = vTr + P;                         // [NW][P]
   S* vec0 = red + NW * P;
   S* vec1 = vec0 + P;
   S* vec2 = vec1 + P;
@@ -245,6 +247,13 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
     __syncthreads();
   };
+  // v~ history rows: global (written by the forward) -> shared slots by
+  // cp.async, zero-filled past column m-1
+  auto vrow = [&](int t) -> S* { return vr + (t & 3) * P; };
+  auto load_row = [&](S* dst, int t) {
+    for (int k = tid; k < P; k += NT) cp_async_zfill(dst + k, hu + size_t(t) * m + (k < m ? k : 0), k < m);
+    cp_async_commit();
+  };
   // coalesced element-wise visit of this CTA's cells: f(local cell e, vector slot or -1)
   auto foreach_cell = [&](auto&& f) {
     if (vec_ok) {
@@ -272,10 +281,10 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     // tolerance-mode continuation / finish) of this CTA's items ----
     if (tid < m) vec1[tid] = a.beta[size_t(u) * m + tid];
     for (int i = tid; i < nloc; i += NT) rowA[i] = a.alpha[size_t(u) * n + r0 + i];
-    for (int idx = tid; idx < (Th + 1) * P; idx += NT) {
-      const int t = idx / P, k = idx - t * P;
-      vh[idx] = k < m ? hu[size_t(t) * m + k] : S(0);
-    }
+    load_row(vTr, Th);
+    load_row(vrow(Th - 1), Th - 1);
+    if (Th >= 2) load_row(vrow(Th - 2), Th - 2);
+    cp_async_wait_all();
     __syncthreads();
     foreach_cell([&](int e0, int q) {
       int i = e0 / m, k = e0 - i * m;
@@ -294,11 +303,11 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     __syncthreads();
     S vT[MC];
 #pragma unroll
-    for (int j = 0; j < MC; ++j) vT[j] = vh[size_t(Th) * P + col(j)];
+    for (int j = 0; j < MC; ++j) vT[j] = vTr[col(j)];
     {
       S vT1[MC];
 #pragma unroll
-      for (int j = 0; j < MC; ++j) vT1[j] = vh[size_t(Th - 1) * P + col(j)];
+      for (int j = 0; j < MC; ++j) vT1[j] = vrow(Th - 1)[col(j)];
       for (int r = 0; r < R; ++r) {   // u~^T (all lanes of the group agree)
         S kr[MC];
         ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * P + g * MC);
@@ -316,12 +325,12 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
           V16<S> t;
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(Th) * P + k]);
+            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vTr[k]);
             if (++k == m) { k = 0; ++i; }
           }
           reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
         } else {
-          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vh[size_t(Th) * P + k]);
+          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vTr[k]);
         }
       });
     };
@@ -351,7 +360,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
     if (phase == PHASE_FWD_CONT) {
       // tolerance mode: continue this step's forward from v~^{t0}, t0 = Th
-      if (tid < P) vec0[tid] = vh[size_t(Th) * P + tid];
+      if (tid < P) vec0[tid] = vTr[tid];
       __syncthreads();
       goto forward_iterations;
     }
@@ -386,15 +395,19 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         gsum = group_sum<S, CG>(gsum);
         if (g == 0) rowB[il] = gsum;
       }
-      reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k)); });
+      reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vTr[k], tot), inv_mass(k)); });
     }
     for (int t = Th; t >= 1; --t) {
+      // stream row t-3 into the slot row t+1 held (last read at level t+2)
+      if (t >= 3) load_row(vrow(t - 3), t - 3);
       S cv[MC], vp[MC], vpp[MC], c[MC];
+      const S* rp = vrow(t - 1);
+      const S* rpp = vrow(t >= 2 ? t - 2 : 0);
 #pragma unroll
       for (int j = 0; j < MC; ++j) {
         cv[j] = vec0[col(j)];
-        vp[j] = vh[size_t(t - 1) * P + col(j)];
-        vpp[j] = vh[size_t(t >= 2 ? t - 2 : 0) * P + col(j)];
+        vp[j] = rp[col(j)];
+        vpp[j] = rpp[col(j)];
         c[j] = S(0);
       }
       const bool first = t == Th;
@@ -416,8 +429,9 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         ut[r] = (ok(r) && t >= 2) ? F::rcp_fast(den) : S(0);
       }
       if (t >= 2) {
+        cp_async_wait_all();   // row t-3 lands before the reduction's barrier publishes it
         reduce_cols(c, [&](int k, S tot) {
-          const S vpk = vh[size_t(t - 1) * P + k];
+          const S vpk = rp[k];
           vec0[k] = mul_(mul_(vpk, -mul_(vpk, tot)), inv_mass(k));
         });
       }
@@ -439,7 +453,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       }
       st_seg<S, MC>(Kt + size_t(il) * P + g * MC, gk);
     }
-    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vh[size_t(Th) * P + tid])) : S(0);
+    if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vTr[tid])) : S(0);
     __syncthreads();
     // ---- Adam ascent on this CTA's cells ----
     const int s = a.state[ST_STEP];

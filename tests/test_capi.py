@@ -41,7 +41,7 @@ def test_library_is_sm100a_only():
 @pytest.mark.parametrize("dtype,n,m,T", [(0, 500, 11, 100), (0, 1000, 21, 100), (0, 2000, 11, 50),
                                           (1, 50, 11, 50), (1, 500, 11, 100), (0, 7, 4, 9), (1, 65, 30, 6),
                                           (0, 4000, 51, 200), (0, 8000, 51, 20), (1, 2000, 51, 20),
-                                          (1, 2048, 11, 100)])
+                                          (1, 2048, 11, 100), (1, 2000, 51, 500), (0, 4000, 51, 500)])
 def test_supported_variants(dtype, n, m, T):
     assert _lib.load().nsw_supported(dtype, n, m, T) == 1
 

@@ -140,3 +140,22 @@ def test_cluster16_fp32_large_n():
     xo, tro, _ = orc.solve(rel, expo, p)
     assert np.abs(xd - xo).max() <= 1e-4
     assert np.abs(np.array(trd.objective) / np.array(tro.objective) - 1).max() <= 1e-6
+
+
+def test_cluster_fp64_tolerance_long_budget_vs_oracle():
+    """float64 cluster tile with the reference's default iteration budget
+    (500): the v~ history is streamed through a 4-row ring, so shared memory
+    does not grow with T."""
+    rng = np.random.default_rng(12)
+    U, n, m = 2, 1200, 40
+    rel = np.clip(rng.uniform(0.05, 1.0, (U, n)), 1e-6, 1.0)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    p = orc.SolverParams(epsilon=0.2, sinkhorn_max_iters=500, sinkhorn_tol=1e-6, outer_max_iters=3,
+                         grad_threshold=1e-300, fixed_schedule=False)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    cfg = SolverConfig(epsilon=0.2, sinkhorn_max_iters=500, sinkhorn_tol=1e-6, outer_max_iters=3,
+                       grad_threshold=1e-300)
+    pol, trd = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg,
+                                  DeviceOptions(dtype="float64", schedule="tolerance"))
+    assert trd.sinkhorn_iterations == tro.sinkhorn_iterations
+    assert np.abs(pol.values - xo).max() <= 1e-9
