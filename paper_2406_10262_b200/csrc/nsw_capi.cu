@@ -469,11 +469,13 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     return fail(NSW_ERR_ARG, "bad schedule");
   const int T = config->sinkhorn_max_iters;
   const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
-  if (const char* e = std::getenv("NSW_MAIN_TILE"); e && var && var->CL == 1) {   // experiments: "R,NT"
-    int r = 0, nt = 0;
-    if (std::sscanf(e, "%d,%d", &r, &nt) == 2)
+  if (const char* e = std::getenv("NSW_MAIN_TILE"); e && var && var->CL == 1) {   // experiments: "R,NT[,MINB]"
+    int r = 0, nt = 0, mb = 0;
+    if (std::sscanf(e, "%d,%d,%d", &r, &nt, &mb) >= 2)
       for (auto& v : variant_registry())
-        if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n) var = &v;
+        if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n &&
+            (mb == 0 || v.minb == mb))
+          var = &v;
   }
   if (!var)
     return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +

@@ -93,6 +93,32 @@ struct Fp<double> {
   static constexpr int kVec = 2;
 };
 
+// Packed fp32 FMA (sm_100 FFMA2, fma.rn.f32x2): two independent IEEE fmas
+// per instruction, d = a * b + c lane-wise -- the same rounding as two FFMAs,
+// half the issue slots.  A scalar b (b0 == b1) becomes FFMA2's broadcast
+// operand form.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0,
+                                      float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
+// c[k] += x[k] * s over an M-vector (packed pairs in fp32, IEEE fma each).
+template <typename S, int M>
+__device__ __forceinline__ void axpy_(S (&c)[M], const S (&x)[M], S s) {
+  if constexpr (sizeof(S) == 4) {
+#pragma unroll
+    for (int k = 0; k + 1 < M; k += 2) ffma2(c[k], c[k + 1], x[k], x[k + 1], s, s, c[k], c[k + 1]);
+    if constexpr (M % 2) c[M - 1] = fmaf(x[M - 1], s, c[M - 1]);
+  } else {
+#pragma unroll
+    for (int k = 0; k < M; ++k) c[k] = fma(x[k], s, c[k]);
+  }
+}
+
 // Padded row pitch (elements) of a K~ row in shared memory: 16-byte multiple.
 template <typename S, int M>
 struct Pitch {

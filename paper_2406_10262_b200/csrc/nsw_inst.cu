@@ -13,7 +13,7 @@
 #define NSW_REG_TC(R, NT, MINB)                                                                        \
   Registrar NSW_CAT(regtc_, __LINE__)(Variant{2, NSW_M, R, NT,                                         \
                                               (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB, true>, \
-                                              &smem_tc_of<R, NT>, 1, 0, MINB});
+                                              &smem_tc_of<R, NT, MINB>, 1, 0, MINB});
 
 #if NSW_F64
 #define NSW_S double
@@ -26,13 +26,13 @@
 namespace nsw {
 namespace {
 
-template <int R, int NT>
+template <int R, int NT, int MINB>
 size_t smem_of(int T) {
-  return step_smem_bytes<NSW_S, NSW_M, R, NT>(T);
+  return step_smem_bytes<NSW_S, NSW_M, R, NT, MINB>(T);
 }
-template <int R, int NT>
+template <int R, int NT, int MINB>
 size_t smem_tc_of(int T) {
-  return step_smem_bytes<NSW_S, NSW_M, R, NT, true>(T);
+  return step_smem_bytes<NSW_S, NSW_M, R, NT, MINB, true>(T);
 }
 
 #define NSW_CAT2(a, b) a##b
@@ -40,7 +40,7 @@ size_t smem_tc_of(int T) {
 #define NSW_REG(R, NT, MINB)                                                                        \
   Registrar NSW_CAT(reg_, __LINE__)(Variant{NSW_DT, NSW_M, R, NT,                                   \
                                             (const void*)&step_kernel<NSW_S, NSW_M, R, NT, MINB>, \
-                                            &smem_of<R, NT>, 1, 0, MINB});
+                                            &smem_of<R, NT, MINB>, 1, 0, MINB});
 
 #if NSW_F64
 // parity instantiation: shapes up to 2048 (M <= 16) / 1024 (M <= 32) items
@@ -66,6 +66,7 @@ NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 6)
 NSW_REG(8, 64, 6)
+NSW_REG(8, 64, 7)   // 7 per SM (register-lean, no input staging): 1036 users per wave
 NSW_REG(4, 128, 3)
 NSW_REG(4, 128, 4)   // 4 per SM: one wave of up to 592 users (strong-scaling shards)
 NSW_REG(8, 128, 3)

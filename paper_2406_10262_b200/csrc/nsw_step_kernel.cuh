@@ -64,8 +64,16 @@ __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a,
 // CH = 2: two interleaved FMA chains (short latency for tiles with few rows
 // per thread); CH = 1: one chain (tiles with >= 4 independent rows per thread
 // have ILP to spare, and the chains' final add is saved).
+// fp32: always two chains, packed into one FFMA2 per column pair.
 template <typename S, int M, int CH = 2>
 __device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
+  if constexpr (sizeof(S) == 4) {
+    S s0 = S(0), s1 = S(0);
+#pragma unroll
+    for (int k = 0; k + 1 < M; k += 2) ffma2(s0, s1, x[k], x[k + 1], y[k], y[k + 1], s0, s1);
+    if constexpr (M % 2) s0 = fmaf(x[M - 1], y[M - 1], s0);
+    return s0 + s1;
+  }
   if constexpr (CH == 1) {
     S s0 = S(0);
 #pragma unroll
@@ -97,12 +105,20 @@ struct RowSlots {
   static constexpr bool kPad = P > M;
 };
 
-template <typename S, int M, int R, int NT, bool TC = false>
+// fp32 tiles of >= 2 warps stage relevance and 1/Imp per row in shared
+// memory; fp64, one-warp and 7-per-SM tiles keep that shared memory free
+// (7 x 34 KB would not fit an SM).
+template <typename S, int NT, int MINB>
+__host__ __device__ constexpr bool stage_inputs() {
+  return sizeof(S) == 4 && NT >= 64 && MINB < 7;
+}
+
+template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = Pitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
-                      size_t(NT / 32) + 4 + (sizeof(S) == 4 && NT >= 64 ? 2 * size_t(NT) * R : 0) + P) +
+                      size_t(NT / 32) + 4 + (stage_inputs<S, NT, MINB>() ? 2 * size_t(NT) * R : 0) + P) +
          32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
          (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
 }
@@ -219,8 +235,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // per-item / per-position inputs staged once per launch (the seed, the gK
   // epilogue and the impact terms read them from here, not from global)
   S* relS = reinterpret_cast<S*>((reinterpret_cast<uintptr_t>(redmax + NW) + 15) & ~uintptr_t(15));  // [NT*R] relevance (0 on padding rows)
-  S* impS = relS + (sizeof(S) == 4 && NT >= 64 ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
-  constexpr bool STAGE = sizeof(S) == 4 && NT >= 64;   // fp64 / 1-warp tiles keep their shared memory for rows
+  constexpr bool STAGE = stage_inputs<S, NT, MINB>();
+  S* impS = relS + (STAGE ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
   S* exS = impS + (STAGE ? size_t(NT) * R : 0);   // [P] exposures (0 from column m-1 on)
   double* exD = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(exS + P) + 15) & ~uintptr_t(15));  // [P]
   // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
@@ -726,12 +742,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           }
           const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
           if constexpr (LEAN) lds_vec_nc<S, M>(vp, vpp1);
-  #pragma unroll
-          for (int k = 0; k < M; ++k) {
-            A[r][k] = fma(-ut[r], cv[k], A[r][k]);
-            A[r][k] = fma(-h, vp[k], A[r][k]);
-            if constexpr (!LAST) c[k] = fma(kr[k], h, c[k]);
-          }
+          axpy_<S, M>(A[r], cv, -ut[r]);
+          axpy_<S, M>(A[r], vp, -h);
+          if constexpr (!LAST) axpy_<S, M>(c, kr, h);
           if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
         if constexpr (!LAST) {
@@ -966,11 +979,9 @@ forward_iterations:
           if (lane == 0) redmax[warp] = rmax;
         }
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          c[k] = A[0][k] * ut[0];
+        for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
-          for (int r = 1; r < R; ++r) c[k] = fma(A[r][k], ut[r], c[k]);
-        }
+        for (int r = 0; r < R; ++r) axpy_<S, M>(c, A[r], ut[r]);
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
           const S vn = F::div_fast(mass(k), tot);
           vec0[k] = vn;
