@@ -112,7 +112,8 @@ def load(path: str | None = None):
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = path or LIB_PATH
+    # NSW_LIB_PATH: an A/B build of the same library (build.py --tag); experiments only
+    p = path or os.environ.get("NSW_LIB_PATH") or LIB_PATH
     if not os.path.exists(p):
         raise NativeLibraryError(
             f"{p} not found: build it with `python -m paper_2406_10262_b200.build` (there is no CPU fallback)")

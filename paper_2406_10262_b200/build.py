@@ -45,22 +45,23 @@ def _dep_mtime():
     return max(os.path.getmtime(p) for p in paths if os.path.exists(p))
 
 
-def _jobs():
+def _jobs(build_dir=BUILD):
     jobs = []
     for f64, M in INSTANCES:
         tag = f"inst_{'f64' if f64 else 'f32'}_M{M}"
-        jobs.append((os.path.join(CSRC, "nsw_inst.cu"), os.path.join(BUILD, tag + ".o"),
+        jobs.append((os.path.join(CSRC, "nsw_inst.cu"), os.path.join(build_dir, tag + ".o"),
                      [f"-DNSW_F64={f64}", f"-DNSW_M={M}"]))
     for f64 in (0, 1):
-        jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(BUILD, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
+        jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(build_dir, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
                      [f"-DNSW_F64={f64}"]))
     for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics"):
-        jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(BUILD, name + ".o"), []))
+        jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(build_dir, name + ".o"), []))
     return jobs
 
 
-def _compile(job, force, verbose):
+def _compile(job, force, verbose, defines=()):
     src, obj, extra = job
+    extra = list(extra) + [f"-D{d}" for d in defines]
     if not force and os.path.exists(obj):
         t = os.path.getmtime(obj)
         if t > os.path.getmtime(src) and t > _dep_mtime():
@@ -74,28 +75,33 @@ def _compile(job, force, verbose):
     return obj, "built", p.stderr
 
 
-def build(jobs: int | None = None, force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
-    work = _jobs()
+def build(jobs: int | None = None, force: bool = False, verbose: bool = False, tag: str = "",
+          defines: tuple = ()) -> str:
+    """Build the library; `tag` + `defines` make an A/B variant
+    (libnswrank_b200_<tag>.so, loaded via NSW_LIB_PATH) for experiments."""
+    build_dir = BUILD + (f"_{tag}" if tag else "")
+    lib = LIB if not tag else os.path.join(HERE, f"libnswrank_b200_{tag}.so")
+    os.makedirs(build_dir, exist_ok=True)
+    work = _jobs(build_dir)
     n = jobs or max(1, min(len(work), os.cpu_count() or 4))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=n) as ex:
-        for obj, status, log in ex.map(lambda j: _compile(j, force, verbose), work):
+        for obj, status, log in ex.map(lambda j: _compile(j, force, verbose, defines), work):
             logs.append((obj, status, log))
     objs = [o for o, _, _ in logs]
     newest = max(os.path.getmtime(o) for o in objs)
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < newest:
-        tmp = LIB + ".tmp"
+    if force or not os.path.exists(lib) or os.path.getmtime(lib) < newest:
+        tmp = lib + ".tmp"
         cmd = [_nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr}")
-        os.replace(tmp, LIB)
+        os.replace(tmp, lib)
     if verbose:
         for obj, status, log in logs:
             if status == "built":
                 print(f"== {os.path.basename(obj)}\n{log}")
-    return LIB
+    return lib
 
 
 def main(argv=None):
@@ -103,8 +109,10 @@ def main(argv=None):
     ap.add_argument("-j", type=int, default=None)
     ap.add_argument("--force", action="store_true")
     ap.add_argument("-v", action="store_true")
+    ap.add_argument("--tag", default="", help="A/B variant name (libnswrank_b200_<tag>.so)")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra preprocessor definition")
     a = ap.parse_args(argv)
-    print(build(a.j, a.force, a.v))
+    print(build(a.j, a.force, a.v, a.tag, tuple(a.defines)))
 
 
 if __name__ == "__main__":

@@ -106,10 +106,16 @@ __device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, 
       : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
 }
 
-// c[k] += x[k] * s over an M-vector (packed pairs in fp32, IEEE fma each).
-template <typename S, int M>
+// NSW_FFMA2=0 builds the scalar-FFMA form of the same loops (A/B experiments).
+#ifndef NSW_FFMA2
+#define NSW_FFMA2 1
+#endif
+
+// c[k] += x[k] * s over an M-vector (IEEE fma each; PK: fp32 pairs packed
+// into FFMA2).
+template <typename S, int M, bool PK = false>
 __device__ __forceinline__ void axpy_(S (&c)[M], const S (&x)[M], S s) {
-  if constexpr (sizeof(S) == 4) {
+  if constexpr (sizeof(S) == 4 && NSW_FFMA2 && PK) {
 #pragma unroll
     for (int k = 0; k + 1 < M; k += 2) ffma2(c[k], c[k + 1], x[k], x[k + 1], s, s, c[k], c[k + 1]);
     if constexpr (M % 2) c[M - 1] = fmaf(x[M - 1], s, c[M - 1]);

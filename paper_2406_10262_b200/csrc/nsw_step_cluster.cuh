@@ -420,12 +420,9 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         const S den = rdot_g<S, MC, CG>(kr, vpp);
         const S gs = first ? rowB[il] : S(0);
         const S h = ut[r] * (gs - ut[r] * sig);
-#pragma unroll
-        for (int j = 0; j < MC; ++j) {
-          A[r][j] = fma(-ut[r], cv[j], A[r][j]);
-          A[r][j] = fma(-h, vp[j], A[r][j]);
-          c[j] = fma(kr[j], h, c[j]);
-        }
+        axpy_<S, MC>(A[r], cv, -ut[r]);
+        axpy_<S, MC>(A[r], vp, -h);
+        axpy_<S, MC>(c, kr, h);
         ut[r] = (ok(r) && t >= 2) ? F::rcp_fast(den) : S(0);
       }
       if (t >= 2) {
@@ -588,11 +585,9 @@ forward_iterations:
         ut[r] = ok(r) ? rp : S(0);
       }
 #pragma unroll
-      for (int j = 0; j < MC; ++j) {
-        c[j] = A[0][j] * ut[0];
+      for (int j = 0; j < MC; ++j) c[j] = S(0);
 #pragma unroll
-        for (int r = 1; r < R; ++r) c[j] = fma(A[r][j], ut[r], c[j]);
-      }
+      for (int r = 0; r < R; ++r) axpy_<S, MC>(c, A[r], ut[r]);
       if constexpr (TOLM) {
         const bool rec = t > t_start;   // residual of iteration t-1 completes here
         S rcta = S(0), rall = S(0);

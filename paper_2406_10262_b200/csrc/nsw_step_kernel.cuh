@@ -64,10 +64,10 @@ __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a,
 // CH = 2: two interleaved FMA chains (short latency for tiles with few rows
 // per thread); CH = 1: one chain (tiles with >= 4 independent rows per thread
 // have ILP to spare, and the chains' final add is saved).
-// fp32: always two chains, packed into one FFMA2 per column pair.
-template <typename S, int M, int CH = 2>
+// PK (fp32): two chains packed into one FFMA2 per column pair.
+template <typename S, int M, int CH = 2, bool PK = false>
 __device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
-  if constexpr (sizeof(S) == 4) {
+  if constexpr (sizeof(S) == 4 && NSW_FFMA2 && PK) {
     S s0 = S(0), s1 = S(0);
 #pragma unroll
     for (int k = 0; k + 1 < M; k += 2) ffma2(s0, s1, x[k], x[k + 1], y[k], y[k + 1], s0, s1);
@@ -214,6 +214,11 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   constexpr int NW = NT / 32;
   constexpr int V = 16 / sizeof(S);
   constexpr int CH = R >= 4 ? 1 : 2;   // row-dot chains; one value for every u~ (forward, replay, u~^T)
+  // Packed FFMA2 in the hot loops for tiles of >= 12 warps per SM (issue-
+  // bound: config 1 main wave) and the 2-row latency tiles (config-1 tail);
+  // the 4- and 8-row tiles at one CTA per SM lose 5-8 % with it (configs 2,
+  // 3; profiles/r01d_ab_ffma2.txt).
+  constexpr bool PK = sizeof(S) == 4 && (NT * MINB >= 384 || R <= 2);
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
   // re-read from shared memory per row instead of held across the row loop
   constexpr bool LEAN = MINB >= 7;
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (int i = tid; i < NT * R; i += NT) {
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        slotA(i) = i < n ? F::rcp_fast(rdot<S, M, CH>(kr, vT1)) : S(0);   // u~^T
+        slotA(i) = i < n ? F::rcp_fast(rdot<S, M, CH, PK>(kr, vT1)) : S(0);   // u~^T
       }
     }
     const int improved = a.state[ST_IMPROVED];
@@ -557,8 +562,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int i = tid + r * NT;
-          const S sig = rdot<S, M, CH>(Kr[r], cv);
-          const S den = rdot<S, M, CH>(Kr[r], vpp);
+          const S sig = rdot<S, M, CH, PK>(Kr[r], cv);
+          const S den = rdot<S, M, CH, PK>(Kr[r], vpp);
           S gs = S(0);
           if (first) {
             gs = slotB(i);
@@ -732,19 +737,19 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           const int i = tid + r * NT;
           S kr[M];
           lds_vec<S, M>(kr, Kt + size_t(i) * P);
-          const S sig = rdot<S, M, CH>(kr, cv);
+          const S sig = rdot<S, M, CH, PK>(kr, cv);
           S den = S(1);
           if constexpr (!LAST) {
             S vpp[M];
             if constexpr (LEAN) lds_vec_nc<S, M>(vpp, vppp);
             else lds_vec<S, M>(vpp, vppp);
-            den = rdot<S, M, CH>(kr, vpp);
+            den = rdot<S, M, CH, PK>(kr, vpp);
           }
           const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
           if constexpr (LEAN) lds_vec_nc<S, M>(vp, vpp1);
-          axpy_<S, M>(A[r], cv, -ut[r]);
-          axpy_<S, M>(A[r], vp, -h);
-          if constexpr (!LAST) axpy_<S, M>(c, kr, h);
+          axpy_<S, M, PK>(A[r], cv, -ut[r]);
+          axpy_<S, M, PK>(A[r], vp, -h);
+          if constexpr (!LAST) axpy_<S, M, PK>(c, kr, h);
           if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
         if constexpr (!LAST) {
@@ -970,7 +975,7 @@ forward_iterations:
         S rmax = S(0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const S sr = rdot<S, M, CH>(A[r], vv);
+          const S sr = rdot<S, M, CH, PK>(A[r], vv);
           if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
           ut[r] = rcp_clamped(sr);
         }
@@ -981,7 +986,7 @@ forward_iterations:
 #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
-        for (int r = 0; r < R; ++r) axpy_<S, M>(c, A[r], ut[r]);
+        for (int r = 0; r < R; ++r) axpy_<S, M, PK>(c, A[r], ut[r]);
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
           const S vn = F::div_fast(mass(k), tot);
           vec0[k] = vn;
@@ -1014,7 +1019,7 @@ forward_iterations:
       S rmax = S(0);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M, CH>(A[r], vv) - S(1)));
+        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M, CH, PK>(A[r], vv) - S(1)));
       rmax = warp_max(rmax);
       if (lane == 0) redmax[warp] = rmax;
       __syncthreads();

@@ -62,6 +62,23 @@ __global__ void k_ffma_dot(float* out, float x0, float y0) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// dependent-chain latency (one warp): cycles per FFMA / FFMA2 in a chain
+__global__ void k_lat(float* out, long long* cyc, float x0) {
+  float a = x0 + threadIdx.x, b = x0 * 0.5f;
+  unsigned long long a2, b2;
+  { float2 t = make_float2(a, a + 1), u = make_float2(b, b); a2 = *reinterpret_cast<unsigned long long*>(&t);
+    b2 = *reinterpret_cast<unsigned long long*>(&u); }
+  long long t0 = clock64();
+#pragma unroll
+  for (int i = 0; i < 256; ++i) asm volatile("fma.rn.f32 %0, %0, %1, %1;" : "+f"(a) : "f"(b));
+  long long t1 = clock64();
+#pragma unroll
+  for (int i = 0; i < 256; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %1;" : "+l"(a2) : "l"(b2));
+  long long t2 = clock64();
+  out[threadIdx.x] = a + __uint_as_float(unsigned(a2));
+  if (threadIdx.x == 0) { cyc[0] = t1 - t0; cyc[1] = t2 - t1; }
+}
+
 template <typename K>
 void run(const char* name, K kern, float* d, int blocks, int threads, double flops_per_inst, int clk_khz, int sms) {
   cudaEvent_t a, b;
@@ -83,6 +100,10 @@ int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   int clk; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
   float* d; cudaMalloc(&d, 1 << 26);
+  long long* cyc; cudaMallocManaged(&cyc, 16);
+  k_lat<<<1, 32>>>(d, cyc, 1.0f); cudaDeviceSynchronize();
+  k_lat<<<1, 32>>>(d, cyc, 1.0f); cudaDeviceSynchronize();
+  printf("dependent chain: FFMA %.2f cycles, FFMA2 %.2f cycles\n", cyc[0] / 256.0, cyc[1] / 256.0);
   for (int t : {128, 256, 512}) {
     int blocks = p.multiProcessorCount * (1024 / t);
     run("ffma", k_ffma, d, blocks, t, 1.0, clk, p.multiProcessorCount);
