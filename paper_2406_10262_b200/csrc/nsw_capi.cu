@@ -477,6 +477,14 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
             (mb == 0 || v.minb == mb))
           var = &v;
   }
+  if (const char* e = std::getenv("NSW_CL_TILE"); e && var && var->CL > 1) {   // experiments: "M,R,NT,CL"
+    int mm = 0, r = 0, nt = 0, cl = 0;
+    if (std::sscanf(e, "%d,%d,%d,%d", &mm, &r, &nt, &cl) == 4)
+      for (auto& v : variant_registry())
+        if (v.dtype == var->dtype && v.M == mm && v.M >= m && v.R == r && v.NT == nt && v.CL == cl &&
+            v.CL * v.rows >= n)
+          var = &v;
+  }
   if (!var)
     return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +
                                          " n=" + std::to_string(n) + " m=" + std::to_string(m) +

@@ -16,23 +16,34 @@
 namespace nsw {
 namespace {
 
-template <int CL>
+template <int MC, int CG, int R, int NT, int CL>
 size_t cl_smem_of(int T) {
-  return cl_smem_bytes<NSW_S, 13, 4, NSW_R, 256, CL>(T);
+  return cl_smem_bytes<NSW_S, MC, CG, R, NT, CL>(T);
 }
 
 #define NSW_CAT2(a, b) a##b
 #define NSW_CAT(a, b) NSW_CAT2(a, b)
-#define NSW_REG_CL(CLS)                                                                                        \
-  Registrar NSW_CAT(regcl_, __LINE__)(Variant{NSW_DT, 52, NSW_R, 256,                                          \
-                                              (const void*)&step_kernel_cl<NSW_S, 13, 4, NSW_R, 256, CLS>,     \
-                                              &cl_smem_of<CLS>, CLS, ClTile<NSW_S, 13, 4, NSW_R, 256, CLS>::NR});
+// (MC columns x CG lanes per row group, R rows per thread, NT threads, CL CTAs
+// per user, MINB CTAs per SM)
+#define NSW_REG_CLT(MC, CG, R, NT, CLS, MINB)                                                              \
+  Registrar NSW_CAT(regcl_, __LINE__)(Variant{NSW_DT, MC * CG, R, NT,                                     \
+                                              (const void*)&step_kernel_cl<NSW_S, MC, CG, R, NT, CLS, MINB>, \
+                                              &cl_smem_of<MC, CG, R, NT, CLS>, CLS,                        \
+                                              ClTile<NSW_S, MC, CG, R, NT, CLS>::NR, MINB});
+#define NSW_REG_CL(CLS) NSW_REG_CLT(13, 4, NSW_R, 256, CLS, 1)
 
 NSW_REG_CL(1)
 NSW_REG_CL(2)
 NSW_REG_CL(4)
 NSW_REG_CL(8)
 NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8192 (fp32) / 2048 (fp64)
+#if !NSW_F64
+// two CTAs per SM (16-CTA clusters for n <= 4096): barrier / exchange waits of
+// one CTA overlap the other's arithmetic
+NSW_REG_CLT(13, 4, 8, 128, 16, 2)
+NSW_REG_CLT(7, 8, 8, 256, 16, 2)
+NSW_REG_CLT(13, 4, 4, 256, 16, 2)
+#endif
 
 }  // namespace
 }  // namespace nsw

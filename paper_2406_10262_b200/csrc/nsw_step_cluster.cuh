@@ -27,13 +27,21 @@ struct ClTile {
   static constexpr int RG = NT / CG;                                  // row groups per CTA
   static constexpr int NR = RG * R;                                   // items per CTA
   static constexpr int NW = NT / 32;
+  // K~ tile layout: each lane's MC-column segment starts on a 16-byte boundary
+  // (vector loads) with an odd number of 16-byte units per segment, so the 8
+  // lanes of a 128-bit load phase (2 row groups x 4 segments) hit distinct
+  // bank quads; KP = CG * SP elements per item row.
+  static constexpr int VE = 16 / sizeof(S);
+  static constexpr int SPV = (MC + VE - 1) / VE;                      // 16-byte units holding MC
+  static constexpr int SP = (SPV % 2 ? SPV : SPV + 1) * VE;           // segment pitch
+  static constexpr int KP = CG * SP;                                  // item-row pitch
 };
 
 template <typename S, int MC, int CG, int R, int NT, int CL>
 __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
   (void)T;   // the v~ history is streamed through a 4-row ring: shared memory does not grow with T
-  return sizeof(S) * (size_t(Tl::NR) * Tl::P + 5 * size_t(Tl::P) + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
+  return sizeof(S) * (size_t(Tl::NR) * Tl::KP + 5 * size_t(Tl::P) + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
                       2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P + 2 * Tl::P + Tl::NW) +
          48;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned) + residual scratch
 }
@@ -109,34 +117,43 @@ __device__ __forceinline__ S group_max(S x) {
 // Row dot of this lane's MC-column segment, completed across the group.
 template <typename S, int MC, int CG>
 __device__ __forceinline__ S rdot_g(const S (&x)[MC], const S (&y)[MC]) {
-  return group_sum<S, CG>(rdot<S, MC>(x, y));
+  return group_sum<S, CG>(rdot<S, MC, 2, true>(x, y));
 }
 
+// A lane's MC-column segment of one item row (16-byte aligned): vector
+// loads / stores, the padding past MC ignored on load and left untouched.
 template <typename S, int MC>
 __device__ __forceinline__ void ld_seg(S (&dst)[MC], const S* src) {
-#pragma unroll
-  for (int j = 0; j < MC; ++j) dst[j] = src[j];
+  lds_vec<S, MC>(dst, src);
 }
 
 template <typename S, int MC>
 __device__ __forceinline__ void st_seg(S* dst, const S (&src)[MC]) {
+  constexpr int VE = 16 / sizeof(S);
 #pragma unroll
-  for (int j = 0; j < MC; ++j) dst[j] = src[j];
+  for (int q = 0; q < MC / VE; ++q) {
+    V16<S> t;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) t.s[e] = src[q * VE + e];
+    reinterpret_cast<V16<S>*>(dst)[q].v = t.v;
+  }
+#pragma unroll
+  for (int j = MC / VE * VE; j < MC; ++j) dst[j] = src[j];
 }
 
-template <typename S, int MC, int CG, int R, int NT, int CL>
-__global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
+template <typename S, int MC, int CG, int R, int NT, int CL, int MINB = 1>
+__global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) {
   using F = Fp<S>;
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
-  constexpr int P = Tl::P, RG = Tl::RG, NR = Tl::NR, NW = Tl::NW;
+  constexpr int P = Tl::P, RG = Tl::RG, NR = Tl::NR, NW = Tl::NW, SP = Tl::SP, KP = Tl::KP;
   constexpr int V = 16 / sizeof(S);
   static_assert(32 % CG == 0 && NT % 32 == 0, "tile shape");
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
-  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][P]
-  S* vr = Kt + size_t(NR) * P;              // [4][P] ring of v~ history rows (row t in slot t & 3)
+  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][CG][SP] item rows in lane segments
+  S* vr = Kt + size_t(NR) * KP;             // [4][P] ring of v~ history rows (row t in slot t & 3)
   S* vTr = vr + 4 * P;                      // [P] row Th of the history (v~ of the solve being differentiated)
   S* red = vTr + P;                         // [NW][P]
   S* vec0 = red + NW * P;
@@ -186,6 +203,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
   const bool vec_ok = (size_t(n) * m % V == 0) && (size_t(NR) * m % V == 0);
   int parity = 0;
   auto lrow = [&](int r) { return rg + r * RG; };
+  auto kx = [&](int i, int k) { return i * KP + (k / MC) * SP + (k % MC); };   // cell (item i, column k)
   auto ok = [&](int r) { return lrow(r) < nloc; };
   auto col = [&](int j) { return g * MC + j; };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
@@ -263,7 +281,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     }
   };
 
-  for (int q = tid; q < NR * P; q += NT) Kt[q] = S(0);
+  for (int q = tid; q < NR * KP; q += NT) Kt[q] = S(0);
   if (tid < P) {
     vec0[tid] = S(0);
     vec1[tid] = S(0);
@@ -293,11 +311,11 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         c.v = reinterpret_cast<const V16<S>*>(Cu)[q].v;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-          Kt[i * P + k] = ktilde(c.s[j], vec1[k], rowA[i]);
+          Kt[kx(i, k)] = ktilde(c.s[j], vec1[k], rowA[i]);
           if (++k == m) { k = 0; ++i; }
         }
       } else {
-        Kt[i * P + k] = ktilde(Cu[e0], vec1[k], rowA[i]);
+        Kt[kx(i, k)] = ktilde(Cu[e0], vec1[k], rowA[i]);
       }
     });
     __syncthreads();
@@ -310,7 +328,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       for (int j = 0; j < MC; ++j) vT1[j] = vrow(Th - 1)[col(j)];
       for (int r = 0; r < R; ++r) {   // u~^T (all lanes of the group agree)
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * P + g * MC);
+        ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * KP + g * SP);
         const S uT = F::rcp_fast(rdot_g<S, MC, CG>(kr, vT1));
         __syncwarp();
         if (g == 0) rowA[lrow(r)] = ok(r) ? uT : S(0);
@@ -325,12 +343,12 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
           V16<S> t;
 #pragma unroll
           for (int j = 0; j < V; ++j) {
-            t.s[j] = mul_(mul_(Kt[i * P + k], rowA[i]), vTr[k]);
+            t.s[j] = mul_(mul_(Kt[kx(i, k)], rowA[i]), vTr[k]);
             if (++k == m) { k = 0; ++i; }
           }
           reinterpret_cast<V16<S>*>(xb)[q].v = t.v;
         } else {
-          xb[e0] = mul_(mul_(Kt[i * P + k], rowA[i]), vTr[k]);
+          xb[e0] = mul_(mul_(Kt[kx(i, k)], rowA[i]), vTr[k]);
         }
       });
     };
@@ -345,7 +363,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
         const double rr = ok(r) ? double(relu[il]) : 0.0;
         const S uT = rowA[il];
         double acc = 0.0;
@@ -377,7 +395,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
         ut[r] = rowA[il];
         const S rr = ok(r) ? relu[il] : S(0);
         const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
@@ -415,14 +433,14 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
         const S sig = rdot_g<S, MC, CG>(kr, cv);
         const S den = rdot_g<S, MC, CG>(kr, vpp);
         const S gs = first ? rowB[il] : S(0);
         const S h = ut[r] * (gs - ut[r] * sig);
-        axpy_<S, MC>(A[r], cv, -ut[r]);
-        axpy_<S, MC>(A[r], vp, -h);
-        axpy_<S, MC>(c, kr, h);
+        axpy_<S, MC, true>(A[r], cv, -ut[r]);
+        axpy_<S, MC, true>(A[r], vp, -h);
+        axpy_<S, MC, true>(c, kr, h);
         ut[r] = (ok(r) && t >= 2) ? F::rcp_fast(den) : S(0);
       }
       if (t >= 2) {
@@ -438,7 +456,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     for (int r = 0; r < R; ++r) {
       const int il = lrow(r);
       S kr[MC], gk[MC];
-      ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+      ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
       const S uT = rowA[il];
       const S rr = ok(r) ? relu[il] : S(0);
       const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
@@ -448,7 +466,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         const S W = (col(j) < m - 1) ? mul_(gx_of(rr, ex[j], imp_i, inv_imp), mul_(mul_(kr[j], uT), vT[j])) : S(0);
         gk[j] = fma(kr[j], A[r][j], W);
       }
-      st_seg<S, MC>(Kt + size_t(il) * P + g * MC, gk);
+      st_seg<S, MC>(Kt + size_t(il) * KP + g * SP, gk);
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vTr[tid])) : S(0);
     __syncthreads();
@@ -479,7 +497,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         vv.v = reinterpret_cast<const V16<S>*>(vu)[q].v;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-          S& slot = Kt[i * P + k];
+          S& slot = Kt[kx(i, k)];
           adam(c.s[j], mm.s[j], vv.s[j], slot);
           slot = mul_(c.s[j], a.nie);
           if (++k == m) { k = 0; ++i; }
@@ -489,7 +507,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
         reinterpret_cast<V16<S>*>(vu)[q].v = vv.v;
       } else {
         S c = Cu[e0], mm = mu[e0], vv = vu[e0];
-        S& slot = Kt[i * P + k];
+        S& slot = Kt[kx(i, k)];
         adam(c, mm, vv, slot);
         slot = mul_(c, a.nie);
         Cu[e0] = c;
@@ -512,7 +530,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       } else {
         c0 = Cu[e];
       }
-      Kt[i * P + k] = mul_(c0, a.nie);
+      Kt[kx(i, k)] = mul_(c0, a.nie);
     }
   }
   __syncthreads();
@@ -531,7 +549,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
     for (int r = 0; r < R; ++r) {
       const int il = lrow(r);
       S kr[MC];
-      ld_seg<S, MC>(kr, Kt + size_t(il) * P + g * MC);
+      ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
       S mx = F::ninf();
 #pragma unroll
       for (int j = 0; j < MC; ++j)
@@ -541,7 +559,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl(const StepArgs<S> a) {
       if (g == 0 && ok(r)) a.alpha[size_t(u) * n + r0 + il] = al;
 #pragma unroll
       for (int j = 0; j < MC; ++j) kr[j] = (ok(r) && col(j) < m) ? F::exp_fast(add_(add_(kr[j], bt[j]), al)) : S(0);
-      st_seg<S, MC>(Kt + size_t(il) * P + g * MC, kr);
+      st_seg<S, MC>(Kt + size_t(il) * KP + g * SP, kr);
     }
   }
   __syncthreads();
@@ -550,7 +568,7 @@ forward_iterations:
   S ut[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    ld_seg<S, MC>(A[r], Kt + size_t(lrow(r)) * P + g * MC);
+    ld_seg<S, MC>(A[r], Kt + size_t(lrow(r)) * KP + g * SP);
     ut[r] = S(0);
   }
   const int t_start = phase == PHASE_FWD_CONT ? Th + 1 : 1;
@@ -587,7 +605,7 @@ forward_iterations:
 #pragma unroll
       for (int j = 0; j < MC; ++j) c[j] = S(0);
 #pragma unroll
-      for (int r = 0; r < R; ++r) axpy_<S, MC>(c, A[r], ut[r]);
+      for (int r = 0; r < R; ++r) axpy_<S, MC, true>(c, A[r], ut[r]);
       if constexpr (TOLM) {
         const bool rec = t > t_start;   // residual of iteration t-1 completes here
         S rcta = S(0), rall = S(0);
