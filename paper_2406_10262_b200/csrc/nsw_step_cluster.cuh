@@ -23,7 +23,8 @@ namespace nsw {
 template <typename S, int MC, int CG, int R, int NT, int CL>
 struct ClTile {
   static constexpr int MP = MC * CG;                                  // padded columns
-  static constexpr int P = (MC % 2) ? MP + 1 : Pitch<S, MP>::value;   // smem pitch
+  // column-vector pitch: >= MP + 1 (tolerance slot), whole 16-byte units
+  static constexpr int P = (MP + 1 + 16 / int(sizeof(S)) - 1) / (16 / int(sizeof(S))) * (16 / int(sizeof(S)));
   static constexpr int RG = NT / CG;                                  // row groups per CTA
   static constexpr int NR = RG * R;                                   // items per CTA
   static constexpr int NW = NT / 32;
@@ -63,6 +64,18 @@ __device__ __forceinline__ void cl_st_async(uint32_t raddr, float v, uint32_t rm
 __device__ __forceinline__ void cl_st_async(uint32_t raddr, double v, uint32_t rmbar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
                "l"(__double_as_longlong(v)), "r"(rmbar)
+               : "memory");
+}
+// 16-byte push (4 floats / 2 doubles of consecutive columns)
+__device__ __forceinline__ void cl_st_async16(uint32_t raddr, const float (&v)[4], uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(raddr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(rmbar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_st_async16(uint32_t raddr, const double (&v)[2], uint32_t rmbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "l"(__double_as_longlong(v[0])), "l"(__double_as_longlong(v[1])), "r"(rmbar)
                : "memory");
 }
 __device__ __forceinline__ void cl_expect_tx(uint32_t mbar, uint32_t bytes) {
@@ -229,21 +242,36 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       if (base + j < lim && c < m) red[warp * P + c] = v[j];
     }
     __syncthreads();
-    S acc = S(0);
-    if (tid < m) {
-      acc = red[tid];
-#pragma unroll
-      for (int w = 1; w < NW; ++w) acc += red[w * P + tid];
-    }
     if constexpr (CL > 1) {
+      // thread q sums columns [VE q, VE q + VE) over the warps (warp order,
+      // the same bits as a per-column sum) and pushes them as one 16-byte
+      // st.async to every CTA of the cluster
+      constexpr int VE = 16 / sizeof(S);
       const uint32_t mb = smem_u32(xmb + parity);
       const int nx = m + (xon ? 1 : 0);
-      if (tid == 0) cl_expect_tx(mb, uint32_t(CL * nx * sizeof(S)));
-      if (tid < nx) {
-        const S mine = tid < m ? acc : xval;
-        const uint32_t slot = smem_u32(xch + (size_t(parity) * CL + rank) * P + tid);
+      const int ng = (nx + VE - 1) / VE;
+      if (tid == 0) cl_expect_tx(mb, uint32_t(CL * ng * 16));
+      if (tid < ng) {
+        V16<S> tot4;
+        tot4.v = reinterpret_cast<const V16<S>*>(red + tid * VE)->v;
 #pragma unroll
-        for (int q = 0; q < CL; ++q) cl_st_async(cl_map(slot, q), mine, cl_map(mb, q));
+        for (int w = 1; w < NW; ++w) {
+          V16<S> x;
+          x.v = reinterpret_cast<const V16<S>*>(red + w * P + tid * VE)->v;
+#pragma unroll
+          for (int e = 0; e < VE; ++e) tot4.s[e] += x.s[e];
+        }
+        S mine[VE];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          const int c = tid * VE + e;
+          mine[e] = c < m ? tot4.s[e] : (c == m && xon ? xval : S(0));
+        }
+        const uint32_t slot = smem_u32(xch + (size_t(parity) * CL + rank) * P + tid * VE);
+#pragma unroll
+        for (int q = 0; q < CL; ++q) cl_st_async16(cl_map(slot, q), mine, cl_map(mb, q));
+      }
+      if (tid < nx) {
         mbar_wait(mb, (xph >> parity) & 1u);
         if (tid < m) {
           S tot = S(0);
@@ -260,6 +288,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       xph ^= 1u << parity;
       parity ^= 1;
     } else {
+      S acc = S(0);
+      if (tid < m) {
+        acc = red[tid];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) acc += red[w * P + tid];
+      }
       if (tid < m) fin(tid, acc);
       if (xon && tid == m) *xmax = xval;
     }
