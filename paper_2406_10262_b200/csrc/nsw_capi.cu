@@ -477,7 +477,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
             (mb == 0 || v.minb == mb))
           var = &v;
   }
-  if (const char* e = std::getenv("NSW_CL_TILE"); e && var && var->CL > 1) {   // experiments: "M,R,NT,CL"
+  if (const char* e = std::getenv("NSW_CL_TILE"); e && var) {   // experiments: "M,R,NT,CL"
     int mm = 0, r = 0, nt = 0, cl = 0;
     if (std::sscanf(e, "%d,%d,%d,%d", &mm, &r, &nt, &cl) == 4)
       for (auto& v : variant_registry())

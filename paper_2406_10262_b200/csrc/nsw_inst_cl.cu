@@ -43,6 +43,9 @@ NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8
 NSW_REG_CLT(13, 4, 8, 128, 16, 2)
 NSW_REG_CLT(7, 8, 8, 256, 16, 2)
 NSW_REG_CLT(13, 4, 4, 256, 16, 2)
+// (one-CTA 2-D tiles with 16-32 warps for configs 2 / 3 -- (6,4,4,1024),
+// (11,2,4,512), (3,4,8,1024), (6,2,8,512) -- ran 9-45 % slower than the row
+// tiles: profiles/r01d_2d_tiles_cfg2_cfg3.txt)
 #endif
 
 }  // namespace
