@@ -64,6 +64,10 @@ __device__ __forceinline__ double add_(double a, double b) { return __dadd_rn(a,
 // CH = 2: two interleaved FMA chains (short latency for tiles with few rows
 // per thread); CH = 1: one chain (tiles with >= 4 independent rows per thread
 // have ILP to spare, and the chains' final add is saved).
+#ifndef NSW_PK_ALL
+#define NSW_PK_ALL 0   // A/B builds: packed FMAs in every fp32 tile
+#endif
+
 // PK (fp32): two chains packed into one FFMA2 per column pair.
 template <typename S, int M, int CH = 2, bool PK = false>
 __device__ __forceinline__ S rdot(const S (&x)[M], const S (&y)[M]) {
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // bound: config 1 main wave) and the 2-row latency tiles (config-1 tail);
   // the 4- and 8-row tiles at one CTA per SM lose 5-8 % with it (configs 2,
   // 3; profiles/r01d_ab_ffma2.txt).
-  constexpr bool PK = sizeof(S) == 4 && (NT * MINB >= 384 || R <= 2);
+  constexpr bool PK = sizeof(S) == 4 && (NT * MINB >= 384 || R <= 2 || NSW_PK_ALL);
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
   // re-read from shared memory per row instead of held across the row loop
   constexpr bool LEAN = MINB >= 7;
