@@ -490,6 +490,44 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
                                          " n=" + std::to_string(n) + " m=" + std::to_string(m) +
                                          " T=" + std::to_string(T));
   CUDA_TRY(cudaSetDevice(options->device));
+  // Cluster tiles: the GPU's GPC layout decides how many clusters of each size
+  // can be resident (B200: 15 clusters of 8 or 9 CTAs, 7 of 16), so among the
+  // tiles that hold n items pick the most users in flight per unit of per-user
+  // time: resident clusters / (rows per thread x CTAs sharing an SM).
+  if (var && var->CL > 1 && options->variant == -1 && !std::getenv("NSW_CL_TILE")) {
+    const Variant* best = nullptr;
+    double best_score = 0.0;
+    for (auto& v : variant_registry()) {
+      if (v.dtype != var->dtype || v.M != var->M || v.CL < 2 || v.CL * v.rows < n || v.smem(T) > kMaxSmem) continue;
+      if (v.CL > 8 && cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+        continue;
+      if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v.smem(T))) != cudaSuccess)
+        continue;
+      cudaLaunchConfig_t lc = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = unsigned(v.CL);
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      lc.gridDim = dim3(unsigned(v.CL) * 64u);
+      lc.blockDim = dim3(unsigned(v.NT));
+      lc.dynamicSmemBytes = v.smem(T);
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      int clusters = 0;
+      if (cudaOccupancyMaxActiveClusters(&clusters, v.fn, &lc) != cudaSuccess || clusters <= 0) continue;
+      int per_sm = 1;   // CTAs sharing an SM run their rows at a fraction of its issue rate
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, v.fn, v.NT, v.smem(T)) != cudaSuccess || per_sm < 1)
+        per_sm = 1;
+      const double score = double(clusters) / (double(v.R) * per_sm);
+      if (!best || score > best_score * 1.0001) {
+        best = &v;
+        best_score = score;
+      }
+    }
+    cudaGetLastError();   // a rejected candidate must not leave a sticky error behind
+    if (best) var = best;
+  }
   if (nsw_status pe = keep_pool_memory(options->device); pe != NSW_OK) return pe;
   auto* s = new nsw_solver();
   if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {

@@ -38,6 +38,9 @@ NSW_REG_CL(4)
 NSW_REG_CL(8)
 NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8192 (fp32) / 2048 (fp64)
 #if !NSW_F64
+// 9-CTA clusters of 448 items (n <= 4032, config 4): B200's GPCs hold 15
+// resident 8- or 9-CTA clusters, so 9 x 15 = 135 SMs work instead of 120
+NSW_REG_CLT(13, 4, 7, 256, 9, 1)
 // two CTAs per SM (16-CTA clusters for n <= 4096): barrier / exchange waits of
 // one CTA overlap the other's arithmetic
 NSW_REG_CLT(13, 4, 8, 128, 16, 2)

@@ -40,10 +40,14 @@ def test_cluster_fp64_vs_oracle(U, n, m, T, outer, eps):
     assert dx <= 1e-9 and df <= 1e-12
 
 
-def test_cfg4_shape_fp32_one_step():
+@pytest.mark.parametrize("tile,R", [(None, 7), ("52,8,256,8", 8)])
+def test_cfg4_shape_fp32_one_step(tile, R, monkeypatch):
     """Config 4 (n=4000, m=51, eps=0.01, 200 inner iterations), fp32 one-step
     parity from the oracle's state at outer step 1, on one user of the
-    BASELINE generator."""
+    BASELINE generator; the default 9-CTA cluster tile (448 items per CTA)
+    and the 8-CTA tile (512 items per CTA)."""
+    if tile:
+        monkeypatch.setenv("NSW_CL_TILE", tile)
     from paper_2406_10262_b200.data import make_instance
     rel, expo, cfg = make_instance("cfg4", seed=0, user_slice=(0, 1))
     T = cfg.inner_iters
@@ -53,7 +57,7 @@ def test_cfg4_shape_fp32_one_step():
     ref = orc.one_step(rel, expo, st, p)
     scfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=T, outer_max_iters=6, grad_threshold=1e-300)
     s = DeviceSolver(rel, expo, rel.shape[1], expo.size + 1, scfg, F32)
-    assert s.variant()["M"] == 52
+    assert s.variant()["M"] == 52 and s.variant()["R"] == R, s.variant()   # R=7: 9-CTA clusters, R=8: 8-CTA
     s.set("cost", st["cost"])
     s.set("adam_m", st["m"])
     s.set("adam_v", st["v"])
