@@ -79,7 +79,7 @@ def build(jobs: int | None = None, force: bool = False, verbose: bool = False, t
           defines: tuple = ()) -> str:
     """Build the library; `tag` + `defines` make an A/B variant
     (libnswrank_b200_<tag>.so, loaded via NSW_LIB_PATH) for experiments."""
-    build_dir = BUILD + (f"_{tag}" if tag else "")
+    build_dir = BUILD if not tag else os.path.join(os.environ.get("TMPDIR", "/tmp"), f"nswrank_b200_build_{tag}")
     lib = LIB if not tag else os.path.join(HERE, f"libnswrank_b200_{tag}.so")
     os.makedirs(build_dir, exist_ok=True)
     work = _jobs(build_dir)
