@@ -101,9 +101,10 @@ def test_cluster_tolerance_schedule_vs_oracle(U, n, m, eps, chunk):
     assert np.abs(pol.values - xo).max() <= 1e-9
 
 
-def test_cluster_tolerance_fp32_runs():
+@pytest.mark.parametrize("n", [2000, 4000])   # 4-CTA and 9-CTA clusters
+def test_cluster_tolerance_fp32_runs(n):
     rng = np.random.default_rng(5)
-    U, n, m = 3, 2000, 51
+    U, m = 3, 51
     rel = np.clip(rng.uniform(0.05, 1.0, (U, n)), 1e-6, 1.0).astype(np.float32).astype(np.float64)
     expo = 1.0 / np.log2(np.arange(2, m + 1))
     cfg = SolverConfig(epsilon=0.3, sinkhorn_max_iters=200, sinkhorn_tol=1e-5, outer_max_iters=4,
