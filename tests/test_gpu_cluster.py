@@ -164,3 +164,4 @@ def test_cluster_fp64_tolerance_long_budget_vs_oracle():
                                   DeviceOptions(dtype="float64", schedule="tolerance"))
     assert trd.sinkhorn_iterations == tro.sinkhorn_iterations
     assert np.abs(pol.values - xo).max() <= 1e-9
+
