@@ -131,6 +131,17 @@ struct Pitch {
   static constexpr int value = (M + Fp<S>::kVec - 1) / Fp<S>::kVec * Fp<S>::kVec;
 };
 
+// Row pitch of the fused step kernel's K~ tile: fp32 rows span an odd number
+// of 16-byte units, so the 8 lanes of a 128-bit load phase (8 consecutive
+// rows) hit 8 distinct bank quads (M = 21 with a 24-float pitch was 2-way
+// conflicted; M = 16 / 32 4- / 8-way).  fp64 keeps the tight pitch (its
+// 2048-item parity tiles need the shared memory).
+template <typename S, int M>
+struct RowPitch {
+  static constexpr int U = (M + Fp<S>::kVec - 1) / Fp<S>::kVec;
+  static constexpr int value = sizeof(S) == 4 ? ((U % 2) ? U : U + 1) * Fp<S>::kVec : Pitch<S, M>::value;
+};
+
 struct OpSum {
   template <typename S>
   __device__ __forceinline__ S operator()(S a, S b) const { return a + b; }

@@ -105,7 +105,7 @@ union V16 {
 // column when the row pitch has one (P > M), else in two row buffers.
 template <typename S, int M>
 struct RowSlots {
-  static constexpr int P = Pitch<S, M>::value;
+  static constexpr int P = RowPitch<S, M>::value;
   static constexpr bool kPad = P > M;
 };
 
@@ -119,7 +119,7 @@ __host__ __device__ constexpr bool stage_inputs() {
 
 template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
-  constexpr int P = Pitch<S, M>::value;
+  constexpr int P = RowPitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
                       size_t(NT / 32) + 4 + (stage_inputs<S, NT, MINB>() ? 2 * size_t(NT) * R : 0) + P) +
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // MMAs (fp32 path, 4-warp CTAs, M <= 16) instead of 2 FFMAs per cell-level.
   static_assert(!TC || (sizeof(S) == 4 && NT == 128 && M <= 16 && R <= 4), "tensor-core tile shape");
   using F = Fp<S>;
-  constexpr int P = Pitch<S, M>::value;
+  constexpr int P = RowPitch<S, M>::value;
   constexpr bool PAD = RowSlots<S, M>::kPad;
   constexpr int NW = NT / 32;
   constexpr int V = 16 / sizeof(S);
