@@ -28,21 +28,27 @@ struct ClTile {
   static constexpr int RG = NT / CG;                                  // row groups per CTA
   static constexpr int NR = RG * R;                                   // items per CTA
   static constexpr int NW = NT / 32;
-  // K~ tile layout: each lane's MC-column segment starts on a 16-byte boundary
-  // (vector loads) with an odd number of 16-byte units per segment, so the 8
-  // lanes of a 128-bit load phase (2 row groups x 4 segments) hit distinct
-  // bank quads; KP = CG * SP elements per item row.
+  // K~ tile layout: a lane's MC-column segment is split into its MCM = MC -
+  // MC % VE leading columns, stored 16-byte aligned with an odd number of
+  // 16-byte units per segment (the 8 lanes of a 128-bit load phase -- 2 row
+  // groups x 4 segments -- hit distinct bank quads; KP = CG * SP per item
+  // row), and its TL trailing columns, stored densely after the main block
+  // ([NR][CG][TL]: the 32 lanes' scalar loads hit 32 consecutive words).
   static constexpr int VE = 16 / sizeof(S);
-  static constexpr int SPV = (MC + VE - 1) / VE;                      // 16-byte units holding MC
+  static constexpr int MCM = MC / VE * VE;                            // vector-loaded columns
+  static constexpr int TL = MC - MCM;                                 // trailing columns
+  static constexpr int SPV = MCM / VE;                                // 16-byte units holding MCM
   static constexpr int SP = (SPV % 2 ? SPV : SPV + 1) * VE;           // segment pitch
-  static constexpr int KP = CG * SP;                                  // item-row pitch
+  static constexpr int KP = CG * SP;                                  // item-row pitch (main block)
+  static constexpr int KT = NR * KP + NR * CG * TL;                   // K~ tile elements
+  static_assert(MCM > 0, "segment narrower than a 16-byte unit");
 };
 
 template <typename S, int MC, int CG, int R, int NT, int CL>
 __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
   using Tl = ClTile<S, MC, CG, R, NT, CL>;
   (void)T;   // the v~ history is streamed through a 4-row ring: shared memory does not grow with T
-  return sizeof(S) * (size_t(Tl::NR) * Tl::KP + 5 * size_t(Tl::P) + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
+  return sizeof(S) * (size_t(Tl::KT) + 5 * size_t(Tl::P) + size_t(Tl::NW) * Tl::P + 3 * Tl::P +
                       2 * size_t(Tl::NR) + 2 * Tl::P + 4 + 2 * size_t(CL) * Tl::P + 2 * Tl::P + Tl::NW) +
          48;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned) + residual scratch
 }
@@ -135,23 +141,42 @@ __device__ __forceinline__ S rdot_g(const S (&x)[MC], const S (&y)[MC]) {
 
 // A lane's MC-column segment of one item row (16-byte aligned): vector
 // loads / stores, the padding past MC ignored on load and left untouched.
-template <typename S, int MC>
-__device__ __forceinline__ void ld_seg(S (&dst)[MC], const S* src) {
-  lds_vec<S, MC>(dst, src);
+// A lane's MC-column segment of item row il (main block: 16-byte vectors;
+// trailing columns: scalars from the dense tail block).
+template <typename Tl, typename S, int MC>
+__device__ __forceinline__ void ld_seg(S (&dst)[MC], const S* Kt, int il, int g) {
+  constexpr int VE = Tl::VE, MCM = Tl::MCM, TL = Tl::TL;
+  const S* src = Kt + size_t(il) * Tl::KP + g * Tl::SP;
+#pragma unroll
+  for (int q = 0; q < MCM / VE; ++q) {
+    V16<S> t;
+    t.v = reinterpret_cast<const V16<S>*>(src)[q].v;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) dst[q * VE + e] = t.s[e];
+  }
+  if constexpr (TL > 0) {
+    const S* tl = Kt + size_t(Tl::NR) * Tl::KP + (size_t(il) * (Tl::KP / Tl::SP) + g) * TL;
+#pragma unroll
+    for (int e = 0; e < TL; ++e) dst[MCM + e] = tl[e];
+  }
 }
 
-template <typename S, int MC>
-__device__ __forceinline__ void st_seg(S* dst, const S (&src)[MC]) {
-  constexpr int VE = 16 / sizeof(S);
+template <typename Tl, typename S, int MC>
+__device__ __forceinline__ void st_seg(S* Kt, int il, int g, const S (&src)[MC]) {
+  constexpr int VE = Tl::VE, MCM = Tl::MCM, TL = Tl::TL;
+  S* dst = Kt + size_t(il) * Tl::KP + g * Tl::SP;
 #pragma unroll
-  for (int q = 0; q < MC / VE; ++q) {
+  for (int q = 0; q < MCM / VE; ++q) {
     V16<S> t;
 #pragma unroll
     for (int e = 0; e < VE; ++e) t.s[e] = src[q * VE + e];
     reinterpret_cast<V16<S>*>(dst)[q].v = t.v;
   }
+  if constexpr (TL > 0) {
+    S* tl = Kt + size_t(Tl::NR) * Tl::KP + (size_t(il) * (Tl::KP / Tl::SP) + g) * TL;
 #pragma unroll
-  for (int j = MC / VE * VE; j < MC; ++j) dst[j] = src[j];
+    for (int e = 0; e < TL; ++e) tl[e] = src[MCM + e];
+  }
 }
 
 template <typename S, int MC, int CG, int R, int NT, int CL, int MINB = 1>
@@ -165,8 +190,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int T = a.T;
-  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][CG][SP] item rows in lane segments
-  S* vr = Kt + size_t(NR) * KP;             // [4][P] ring of v~ history rows (row t in slot t & 3)
+  S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][CG][SP] lane segments + [NR][CG][TL] tails
+  S* vr = Kt + size_t(Tl::KT);             // [4][P] ring of v~ history rows (row t in slot t & 3)
   S* vTr = vr + 4 * P;                      // [P] row Th of the history (v~ of the solve being differentiated)
   S* red = vTr + P;                         // [NW][P]
   S* vec0 = red + NW * P;
@@ -216,7 +241,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   const bool vec_ok = (size_t(n) * m % V == 0) && (size_t(NR) * m % V == 0);
   int parity = 0;
   auto lrow = [&](int r) { return rg + r * RG; };
-  auto kx = [&](int i, int k) { return i * KP + (k / MC) * SP + (k % MC); };   // cell (item i, column k)
+  auto kx = [&](int i, int k) {   // cell (item i, column k)
+    const int gg = k / MC, j = k - gg * MC;
+    return j < Tl::MCM ? i * KP + gg * SP + j : NR * KP + (i * CG + gg) * Tl::TL + (j - Tl::MCM);
+  };
   auto ok = [&](int r) { return lrow(r) < nloc; };
   auto col = [&](int j) { return g * MC + j; };
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
@@ -315,7 +343,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
     }
   };
 
-  for (int q = tid; q < NR * KP; q += NT) Kt[q] = S(0);
+  for (int q = tid; q < Tl::KT; q += NT) Kt[q] = S(0);
   if (tid < P) {
     vec0[tid] = S(0);
     vec1[tid] = S(0);
@@ -362,7 +390,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       for (int j = 0; j < MC; ++j) vT1[j] = vrow(Th - 1)[col(j)];
       for (int r = 0; r < R; ++r) {   // u~^T (all lanes of the group agree)
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(lrow(r)) * KP + g * SP);
+        ld_seg<Tl, S, MC>(kr, Kt, lrow(r), g);
         const S uT = F::rcp_fast(rdot_g<S, MC, CG>(kr, vT1));
         __syncwarp();
         if (g == 0) rowA[lrow(r)] = ok(r) ? uT : S(0);
@@ -397,7 +425,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
+        ld_seg<Tl, S, MC>(kr, Kt, il, g);
         const double rr = ok(r) ? double(relu[il]) : 0.0;
         const S uT = rowA[il];
         double acc = 0.0;
@@ -429,7 +457,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
+        ld_seg<Tl, S, MC>(kr, Kt, il, g);
         ut[r] = rowA[il];
         const S rr = ok(r) ? relu[il] : S(0);
         const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
@@ -467,7 +495,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
+        ld_seg<Tl, S, MC>(kr, Kt, il, g);
         const S sig = rdot_g<S, MC, CG>(kr, cv);
         const S den = rdot_g<S, MC, CG>(kr, vpp);
         const S gs = first ? rowB[il] : S(0);
@@ -490,7 +518,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
     for (int r = 0; r < R; ++r) {
       const int il = lrow(r);
       S kr[MC], gk[MC];
-      ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
+      ld_seg<Tl, S, MC>(kr, Kt, il, g);
       const S uT = rowA[il];
       const S rr = ok(r) ? relu[il] : S(0);
       const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
@@ -500,7 +528,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
         const S W = (col(j) < m - 1) ? mul_(gx_of(rr, ex[j], imp_i, inv_imp), mul_(mul_(kr[j], uT), vT[j])) : S(0);
         gk[j] = fma(kr[j], A[r][j], W);
       }
-      st_seg<S, MC>(Kt + size_t(il) * KP + g * SP, gk);
+      st_seg<Tl, S, MC>(Kt, il, g, gk);
     }
     if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vTr[tid])) : S(0);
     __syncthreads();
@@ -583,7 +611,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
     for (int r = 0; r < R; ++r) {
       const int il = lrow(r);
       S kr[MC];
-      ld_seg<S, MC>(kr, Kt + size_t(il) * KP + g * SP);
+      ld_seg<Tl, S, MC>(kr, Kt, il, g);
       S mx = F::ninf();
 #pragma unroll
       for (int j = 0; j < MC; ++j)
@@ -593,7 +621,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       if (g == 0 && ok(r)) a.alpha[size_t(u) * n + r0 + il] = al;
 #pragma unroll
       for (int j = 0; j < MC; ++j) kr[j] = (ok(r) && col(j) < m) ? F::exp_fast(add_(add_(kr[j], bt[j]), al)) : S(0);
-      st_seg<S, MC>(Kt + size_t(il) * KP + g * SP, kr);
+      st_seg<Tl, S, MC>(Kt, il, g, kr);
     }
   }
   __syncthreads();
@@ -602,7 +630,7 @@ forward_iterations:
   S ut[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    ld_seg<S, MC>(A[r], Kt + size_t(lrow(r)) * KP + g * SP);
+    ld_seg<Tl, S, MC>(A[r], Kt, lrow(r), g);
     ut[r] = S(0);
   }
   const int t_start = phase == PHASE_FWD_CONT ? Th + 1 : 1;
