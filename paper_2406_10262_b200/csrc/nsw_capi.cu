@@ -570,6 +570,8 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->partial, size_t(users_local) * n * 8);
   // impact reduction: ~2 CTAs per SM of (8 items x user chunk)
   s->imp_chunks = std::max(1, std::min(std::min(users_local, 64), (2 * sm_count() * IMP_ITEMS + n - 1) / n));
+  if (const char* e = std::getenv("NSW_IMP_CHUNKS"))   // experiments
+    s->imp_chunks = std::max(1, std::min(users_local, std::atoi(e)));
   ALLOC(s->split, size_t(s->imp_chunks) * n * 8);
   ALLOC(s->own_imp_local, size_t(n + 1) * 8);
   ALLOC(s->own_imp_all, size_t(world) * (n + 1) * 8);
