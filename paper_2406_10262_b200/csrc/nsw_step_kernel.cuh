@@ -124,6 +124,7 @@ __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
                       size_t(NT / 32) + 4 + (stage_inputs<S, NT, MINB>() ? 2 * size_t(NT) * R : 0) + P) +
          32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
+         16 +                   // mbarrier of the cost tile's bulk copy
          (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
 }
 
@@ -249,8 +250,9 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* exS = impS + (STAGE ? size_t(NT) * R : 0);   // [P] exposures (0 from column m-1 on)
   double* exD = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(exS + P) + 15) & ~uintptr_t(15));  // [P]
   // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
+  uint64_t* bmb = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(exD + P) + 7) & ~uintptr_t(7));
   unsigned char* tc_base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(exD + P) + 127) & ~uintptr_t(127));
+      (reinterpret_cast<uintptr_t>(bmb + 1) + 127) & ~uintptr_t(127));
   float* Bop = reinterpret_cast<float*>(tc_base);            // [2][2][16 x 8]
   uint64_t* mbar = reinterpret_cast<uint64_t*>(tc_base + 2048);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_base + 2056);
@@ -320,6 +322,31 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // asynchronously (cp.async, zero-filled past column m-1); alpha, beta,
   // relevance and Imp go through registers and are stored after the tile is
   // zeroed.
+  // The user's cost tile (contiguous [n][m], 16-byte multiple) comes in as one
+  // TMA bulk copy (cp.async.bulk, completion on an mbarrier) into the top of
+  // the K~ tile region, issued before anything else; the rebuild expands it
+  // in place into padded K~ rows.
+  // fp32: only the 2048-row tiles (config 3: +1.8 %); on the smaller fp32
+  // tiles the extra code perturbs the hot loops' register allocation for a
+  // -0.3..-0.8 % net (profiles/r01f_ab_tma.txt).  fp64 tiles always use it.
+  constexpr bool BULK_TILE = sizeof(S) == 8 || NT * R >= 2048;
+  const bool bulk = BULK_TILE && rebuild && vec_ok && !TC;
+  const int stage_off = (NT * R * P - nm) / V * V;   // first staged element (16-byte aligned)
+  if (BULK_TILE && bulk && tid == 0) {
+    const uint32_t mb = smem_u32(bmb);
+    const uint32_t bytes = uint32_t(nm) * sizeof(S);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(mb),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(Kt + stage_off)),
+        "l"(Cu), "r"(bytes), "r"(mb)
+        : "memory");
+  }
   if (rebuild) {
     for (int idx = tid; idx < (Th + 1) * P; idx += NT) {
       const int t = idx / P, k = idx - t * P;
@@ -347,14 +374,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (size_t off = size_t(tid) * 128; off < bytes; off += size_t(NT) * 128)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(b + off));
     };
-    pf(Cu, size_t(nm) * sizeof(S));
+    if (!bulk) pf(Cu, size_t(nm) * sizeof(S));
     if (phase == PHASE_RUNNING) {
       pf(mu, size_t(nm) * sizeof(S));
       pf(vu, size_t(nm) * sizeof(S));
     }
   }
-  // zero the tile (padding rows / columns must stay 0) and the small vectors
-  for (int q = tid; q < NT * R * P / V; q += NT) reinterpret_cast<V16<S>*>(Kt)[q].v = V16<S>{}.v;
+  // zero the tile (padding rows / columns must stay 0) and the small vectors;
+  // a bulk-copied tile is rebuilt as whole padded rows instead
+  if (!bulk)
+    for (int q = tid; q < NT * R * P / V; q += NT) reinterpret_cast<V16<S>*>(Kt)[q].v = V16<S>{}.v;
   if (tid < P) {
     vec0[tid] = S(0);
     vec1[tid] = bt0;
@@ -366,7 +395,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int i = tid + r * NT;
-    if (rebuild) slotA(i) = al[r];
+    if (rebuild && !bulk) slotA(i) = al[r];   // (bulk: the staged tile occupies the slots)
     if constexpr (STAGE) {
       relS[i] = rv[r];
       impS[i] = S(1.0 / iv[r]);   // reciprocal: gx is two multiplies
@@ -392,7 +421,30 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   if (rebuild) {
     // ---------------- rebuild K~ from C, alpha, beta (step k-1's for the
     // backward; this step's for a tolerance-mode continuation / finish) ------
-    if (vec_ok) {
+    if (BULK_TILE && bulk) {
+      // this thread's rows from the staged tile into registers, a barrier
+      // (rows expand in place), then whole padded rows; the row's alpha
+      // goes to its padding slot afterwards
+      mbar_wait(smem_u32(bmb), 0u);
+      S cr[R][M];
+      const S* stg = Kt + stage_off;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+#pragma unroll
+        for (int k = 0; k < M; ++k) cr[r][k] = (i < n && k < m) ? stg[i * m + k] : S(0);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = tid + r * NT;
+        S kr[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) kr[k] = (i < n && k < m) ? ktilde(cr[r][k], vec1[k], al[r]) : S(0);
+        sts_vec<S, M>(Kt + size_t(i) * P, kr);
+        slotA(i) = al[r];
+      }
+    } else if (vec_ok) {
       const int nq = nm / V;
       for (int q0 = tid; q0 < nq; q0 += 8 * NT) {
         V16<S> c[8];
