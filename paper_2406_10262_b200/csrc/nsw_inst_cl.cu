@@ -41,11 +41,9 @@ NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8
 // 9-CTA clusters of 448 items (n <= 4032, config 4): B200's GPCs hold 15
 // resident 8- or 9-CTA clusters, so 9 x 15 = 135 SMs work instead of 120
 NSW_REG_CLT(13, 4, 7, 256, 9, 1)
-// two CTAs per SM (16-CTA clusters for n <= 4096): barrier / exchange waits of
-// one CTA overlap the other's arithmetic
-NSW_REG_CLT(13, 4, 8, 128, 16, 2)
-NSW_REG_CLT(7, 8, 8, 256, 16, 2)
-NSW_REG_CLT(13, 4, 4, 256, 16, 2)
+// (two CTAs per SM on 16-CTA clusters -- (13,4,8,128), (7,8,8,256), (13,4,4,256)
+// -- and a 14-warp (13,4,4,448) 9-CTA tile ran 3-19 % slower than the
+// 1-CTA/SM tiles: profiles/r01d_cluster_tile_variants.txt)
 // (one-CTA 2-D tiles with 16-32 warps for configs 2 / 3 -- (6,4,4,1024),
 // (11,2,4,512), (3,4,8,1024), (6,2,8,512) -- ran 9-45 % slower than the row
 // tiles: profiles/r01d_2d_tiles_cfg2_cfg3.txt)
