@@ -19,6 +19,7 @@ _EXPORTS = {
     "ranking": ("top_positions",),
     "metrics": ("user_utility", "mean_max_envy", "items_better_off", "items_worse_off", "policy_metrics"),
     "distributed": ("solve_fair_ranking_distributed", "shard_users"),
+    "experiments": ("compute_policy", "install"),
 }
 
 _ATTR_TO_MODULE = {name: mod for mod, names in _EXPORTS.items() for name in names}
