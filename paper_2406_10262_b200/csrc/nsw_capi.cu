@@ -651,11 +651,13 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, var->fn, var->NT, s->smem);
     const Variant* wide = choose_wide_variant(var, n, T);
-    if (const char* e = std::getenv("NSW_TAIL_TILE")) {   // experiments: "R,NT" of the tail tile
-      int r = 0, nt = 0;
-      if (std::sscanf(e, "%d,%d", &r, &nt) == 2)
+    if (const char* e = std::getenv("NSW_TAIL_TILE")) {   // experiments: "R,NT[,MINB]" of the tail tile
+      int r = 0, nt = 0, mb = 0;
+      if (std::sscanf(e, "%d,%d,%d", &r, &nt, &mb) >= 2)
         for (auto& v : variant_registry())
-          if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n) wide = &v;
+          if (v.dtype == var->dtype && v.M == var->M && v.CL == 1 && v.R == r && v.NT == nt && v.rows >= n &&
+              (mb == 0 || v.minb == mb))
+            wide = &v;
     }
     const int slots = per_sm * sms;
     if (wide && wide != var && slots > 0) {

@@ -70,6 +70,8 @@ NSW_REG(8, 64, 7)   // 7 per SM (register-lean, no input staging): 1036 users pe
 NSW_REG(4, 128, 3)
 NSW_REG(4, 128, 4)   // 4 per SM: one wave of up to 592 users (strong-scaling shards)
 NSW_REG(8, 128, 3)
+// (tail tile capped at 128 / 80 registers to start beside draining main CTAs:
+// 0.4 / 1.2 % slower, profiles/r01g_tail_registers.txt)
 NSW_REG(8, 256, 1)   // (4, 512, 1): 16 warps, 11 % slower on config 3 (profiles/r01d_row_tiles_cfg2_cfg3.txt)
 NSW_REG(2, 256, 1)
 NSW_REG(1, 512, 1)
