@@ -1,6 +1,6 @@
 """Benchmark of the NSW ascent hot path (driver contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
 
 A "step" is one outer ascent iteration of solve_fair_ranking (reference
 solver.py:186-240): one Sinkhorn solve per user (T inner iterations), the
@@ -8,13 +8,21 @@ impact reduction, the unrolled backward and the Adam update, over the whole
 synthetic instance.  Metric: outer ascent iterations / s (BASELINE.json
 "outer ascent iters/sec & Sinkhorn cell-updates/s"), whole job.
 
+Workload: BASELINE config 2 by default (10k users x 1000 items x 21
+positions, eps 0.02, 100 inner iterations) -- the largest BASELINE
+configuration that BASELINE runs at 1/2/4/8 GPUs and that fits one GPU, so
+the 1-GPU bench and the scaling runs measure the same job (users sharded over
+ranks, strong scaling).  ``--config cfg1`` runs the single-GPU config.
+
 Our arm prints one JSON line with value (device-resident, CUDA-event timed,
 L2 flushed between steps), e2e (public API with host buffers), roofline of
 the dominant kernel (the fused step kernel, FP32-pipe bound), cpu_baseline
 (the oracle port on a bounded user slice) and nvidia-smi clocks.
-The reference arm (--impl reference) times the CPU oracle port (the
-reference is pure Python and does not exist on the GPU box) with all host
-cores on a bounded user sample.
+``--gpus N`` outside torchrun re-launches itself under torch.distributed.run
+with one rank per GPU (at most the visible GPU count).
+The reference arm (--impl reference) runs the unmodified reference package
+(``baseline/_ref``, its public ``solve_fair_ranking`` under the fixed-schedule
+shim of SURVEY.md 8(c)) on every host core, one user sample per process.
 """
 
 from __future__ import annotations
@@ -107,6 +115,25 @@ def _dist_env():
     return world, rank, local
 
 
+DEFAULT_CONFIG = "cfg2"
+
+
+def _spawn_ranks(a, argv):
+    """--gpus N outside torchrun: re-launch under torch.distributed.run with
+    one rank per GPU (clamped to the visible GPUs: ranks never share a GPU)."""
+    import socket
+    import torch
+    n = min(a.gpus, max(1, torch.cuda.device_count()))
+    if n <= 1:
+        return None
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
+
+
 # ------------------------------------------------------------------------------
 # CPU baseline: the oracle port (test infrastructure) on a bounded user slice
 # ------------------------------------------------------------------------------
@@ -149,28 +176,55 @@ def cpu_baseline(name, users_per_proc, procs, steps):
             "seconds_per_step": t_full}
 
 
-def _ref_worker(conn, name, start, stop):
-    """Persistent CPU worker: owns a user slice and runs one full outer step
-    of the oracle port (forward, impact, gradient, backward, Adam) per 'step'."""
-    from oracle import nsw_oracle as orc
+REF_DIR = os.path.join(REPO, "baseline", "_ref")
+
+
+def _import_reference():
+    """The unmodified reference package installed at baseline/_ref (pip
+    --target), or None."""
+    if os.path.isdir(os.path.join(REF_DIR, "nswrank")):
+        if REF_DIR not in sys.path:
+            sys.path.insert(0, REF_DIR)
+        try:
+            import nswrank
+            return nswrank
+        except Exception:
+            return None
+    return None
+
+
+def _ref_solve_worker(args):
+    """One process: the reference's public solve_fair_ranking on a user
+    sample, under the fixed-schedule shim (every solve runs exactly
+    sinkhorn_max_iters iterations); returns its own per-step
+    wall times (SolveTrace.wall_time)."""
+    name, start, stop, outer = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    nswrank = _import_reference()
     rel, expo, cfg = make_instance(name, seed=0, user_slice=(start, stop))
     U, n = rel.shape
     m = expo.size + 1
-    row, col, lr, lc = orc.ranking_marginals(n, m)
-    cost = orc.initial_cost(U, n, m, cfg.epsilon)
-    am, av, step = np.zeros_like(cost), np.zeros_like(cost), 0
-    lvi = np.zeros((U, m))
-    gx = np.zeros_like(cost)
-    nie = -1.0 / cfg.epsilon
-    while conn.recv() == "step":
-        K = cost * nie
-        fwd = orc.sinkhorn_forward(K, lr, lc, row, col, -1.0, cfg.inner_iters, lvi)
-        imp = orc.impact(rel, expo, fwd.plan)
-        orc.welfare_gradient(rel, expo, imp, gx)
-        g = orc.sinkhorn_backward(K, lr, lc, fwd.hist, lvi, gx, fwd.plan, fwd.log_u) * nie
-        cost, am, av, step = orc.adam_ascent(cost, g, am, av, step, 0.05, 0.9, 0.999, 1e-8)
-        lvi = fwd.log_v
-        conn.send("done")
+    if nswrank is not None:
+        import nswrank.solver as ref_solver
+        real = ref_solver._sinkhorn_batch
+
+        def fixed(*aa, **kw):
+            kw["tol"] = -1.0
+            r = real(*aa, **kw)
+            r.converged[:] = True
+            return r
+
+        ref_solver._sinkhorn_batch = fixed
+        scfg = nswrank.SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=cfg.inner_iters, outer_max_iters=outer,
+                                    grad_threshold=1e-300)
+        _, tr = nswrank.solve_fair_ranking(nswrank.RelevanceMatrix(rel), nswrank.ExposureModel(expo),
+                                           nswrank.ProblemShape(U, n, m), scfg)
+        return "reference", list(tr.wall_time)
+    from oracle import nsw_oracle as orc   # fallback: the bit-exact port
+    p = orc.SolverParams(epsilon=cfg.epsilon, sinkhorn_max_iters=cfg.inner_iters, outer_max_iters=outer,
+                         grad_threshold=1e-300)
+    _, tr, _ = orc.solve(rel, expo, p)
+    return "port", list(tr.wall_time)
 
 
 def run_reference(a):
@@ -178,53 +232,57 @@ def run_reference(a):
     if rank != 0:
         return 0
     import multiprocessing as mp
-    cores = os.cpu_count() or 1
-    procs = max(1, cores)
+    procs = max(1, os.cpu_count() or 1)
     cfg = BASELINE_CONFIGS[a.config]
-    # ~0.1-0.3 s of CPU work per process per timed step
-    # (the port runs ~1e-7 s per cell per inner iteration for forward+backward)
+    # users per process so that one outer step of a process is ~0.3 s of
+    # numpy work (measured ~45 ns per cell per inner iteration, fwd + bwd)
     users = max(1, min(cfg.num_users // procs,
-                       int(0.2 / (1e-7 * cfg.num_items * cfg.num_positions * cfg.inner_iters))))
-    ctx = mp.get_context("fork")
-    conns, ps = [], []
-    for i in range(procs):
-        pa, pb = ctx.Pipe()
-        p = ctx.Process(target=_ref_worker, args=(pb, a.config, i * users, (i + 1) * users), daemon=True)
-        p.start()
-        conns.append(pa)
-        ps.append(p)
-    samples = []
-    for i in range(a.warmup + a.steps):
-        t0 = time.perf_counter()
-        for c in conns:
-            c.send("step")
-        for c in conns:
-            c.recv()
-        if i >= a.warmup:
-            samples.append(time.perf_counter() - t0)
-    for c in conns:
-        c.send("stop")
-    for p in ps:
-        p.join(timeout=10)
-    t_sample = float(np.mean(samples))
-    t = t_sample * cfg.num_users / (procs * users)
-    v = 1.0 / t
+                       int(0.3 / (45e-9 * cfg.num_items * cfg.num_positions * cfg.inner_iters))))
+    outer = a.warmup + a.steps + 1          # the final step is forward only (solver.py:220-223)
+    jobs = [(a.config, i * users, (i + 1) * users, outer) for i in range(procs)]
+    # the reference as it ships: one process alone (1 core), 1 warm-up + 2 steps
+    with mp.get_context("fork").Pool(1) as pool:
+        _, w1 = pool.map(_ref_solve_worker, [(a.config, 0, users, 4)])[0]
+    one_core_full = float(np.mean(w1[1:3])) * cfg.num_users / users
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(procs) as pool:
+        res = pool.map(_ref_solve_worker, jobs)
+    wall = time.perf_counter() - t0
+    kind = res[0][0]
+    walls = np.array([w for _, w in res])                  # [procs][outer]
+    timed = walls[:, a.warmup:a.warmup + a.steps]          # the K timed full steps
+    sample_step_s = float(timed.max(axis=0).mean())        # all processes done = one sample step
+    users_done = users * procs
+    factor = cfg.num_users / users_done
+    t_full = sample_step_s * factor                        # whole workload, all host cores
+    v = 1.0 / t_full
+    sample = (f"{'baseline/_ref nswrank.solve_fair_ranking (unmodified reference, fixed-schedule shim)' if kind == 'reference' else 'oracle port (reference not installed)'}"
+              f" in {procs} processes x {users} users of {a.config} (float64 numpy, 1 thread each), "
+              f"{a.warmup} warm-up + {a.steps} timed outer steps + 1 final forward; {sample_step_s * 1e3:.1f} ms per "
+              f"sample step, extrapolated x{factor:.1f} to |U|={cfg.num_users}; wall {wall:.1f} s")
     line = {"impl": "reference", "metric": "outer_ascent_iters_per_s", "value": v, "unit": "outer_iters/s",
-            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+            "n_gpus": max(world, a.gpus), "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": sample_step_s * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (BASELINE generator, seed 0)",
-            "config": {"workload": f"{a.config}: U={cfg.num_users} I={cfg.num_items} m={cfg.num_positions} "
-                                   f"eps={cfg.epsilon} T_in={cfg.inner_iters}",
+            "config": {"workload": _workload(a.config, cfg.num_users, cfg.num_items, cfg.num_positions,
+                                             cfg.epsilon, cfg.inner_iters),
                        "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": v, "unit": "outer_iters/s", "cores": procs, "kind": "port",
-                             "sample": f"{procs} processes x {users} users x 1 outer step (fwd+bwd+Adam, "
-                                       f"float64 numpy) per timed step, {t_sample:.3f} s/step, extrapolated "
-                                       f"x{cfg.num_users / (procs * users):.1f} to |U|={cfg.num_users} "
-                                       f"(reference is pure Python; the oracle port stands in since "
-                                       f"/root/reference is absent on the box)"},
+            "extrapolation": {"sample_users": users_done, "factor": factor,
+                              "ms_per_step_full_workload": t_full * 1e3,
+                              "note": "ms_per_step is the measured time of one sample step; value is the "
+                                      "whole-workload rate (fixed-schedule steps do identical work per user)"},
+            "one_core": {"value": 1.0 / one_core_full, "unit": "outer_iters/s",
+                         "note": "the reference alone in one process (it is single-threaded numpy): "
+                                 "its per-step time on the same sample x |U| / sample users"},
+            "cpu_baseline": {"value": v, "unit": "outer_iters/s", "cores": procs, "kind": kind, "sample": sample},
             "e2e": {"value": v, "unit": "outer_iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _workload(name, U, n, m, eps, T):
+    return f"{name}: U={U} I={n} m={m} eps={eps} T_in={T}"
 
 
 # ------------------------------------------------------------------------------
@@ -296,7 +354,11 @@ def run_ours(a):
         t = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in evs)], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
-        ms_fused = float("nan")
+        # per-rank fused-kernel time for the roofline: the fused launches
+        # alone (no exchange), replayed after the timed region, max over ranks
+        tf = torch.tensor([sa.solver.time_fused(a.steps, flush_l2=True)], device="cuda")
+        dist.all_reduce(tf, op=dist.ReduceOp.MAX)
+        ms_fused = float(tf.item())
         variant = sa.solver.variant()
         # the step replays a torch-captured graph: main (+ tail) fused launch,
         # impact reduction and finalize (our kernels) around the NCCL all-gather
@@ -314,14 +376,17 @@ def run_ours(a):
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_total / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if a.dtype == "float32" else "f64",
             "data": "synthetic (BASELINE generator, seed 0)",
-            "config": {"workload": f"{a.config}: U={U} I={n} m={m} eps={cfg.epsilon} T_in={T} (fixed schedule)",
+            "config": {"workload": _workload(a.config, U, n, m, cfg.epsilon, T), "schedule": "fixed (BASELINE)",
                        "users_per_gpu": users_local, "l2": "flushed between timed steps (1 GiB write, then discard of those lines)",
                        "tile": variant},
             "sinkhorn_cell_updates_per_s": cell_updates / (ms_total / 1e3),
             "gpu_launches": launches, "clocks": clocks}
-    if world == 1 and ms_fused == ms_fused:
+    if a.gpus != world:
+        line["requested_gpus"] = a.gpus   # clamped to the visible GPUs (ranks never share a GPU)
+    if ms_fused == ms_fused:
         per_launch_s = ms_fused / 1e3 / a.steps
-        instr = INSTR_PER_CELL_ITER * cells * T
+        cells_rank = users_local * n * m      # one launch processes this rank's users
+        instr = INSTR_PER_CELL_ITER * cells_rank * T
         clk = peaks.get("sm_max_mhz", 1965.0)
         peak = SMS * FP32_LANES_PER_SM_CLK * clk * 1e6
         achieved = instr / per_launch_s
@@ -330,13 +395,14 @@ def run_ours(a):
         if os.path.exists(tfile):
             with open(tfile) as f:
                 traffic = json.load(f).get(f"{a.config}_{a.dtype}")
-        hbm_bytes = (28 if a.dtype == "float32" else 56) * cells
+        hbm_bytes = (28 if a.dtype == "float32" else 56) * cells_rank
         line["roofline"] = {
             "bound": "fp32", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tinstr/s",
             "frac": achieved / peak, "traffic": traffic,
             "kernel": "step_kernel (fused backward+Adam+forward)",
             "count": f"{INSTR_PER_CELL_ITER} FP32-pipe instr per cell per inner iteration (SURVEY 8(d) form B) x "
-                     f"{cells} cells x {T} iterations per launch",
+                     f"{cells_rank} cells x {T} iterations per launch"
+                     + (f" (rank 0 of {world}: per-rank fused time, max over ranks)" if world > 1 else ""),
             "peak_note": f"148 SMs x 128 FP32 lanes x {clk:.0f} MHz (sm_max from MEASURED_PEAKS.json, "
                          f"{peaks_kind}); no measured FP32 peak exists, so the datasheet lane rate is used",
             "fused_ms_per_launch": per_launch_s * 1e3,
@@ -345,7 +411,7 @@ def run_ours(a):
                               "achieved_gbs": hbm_bytes / per_launch_s / 1e9,
                               "peak_gbs": peaks.get("hbm_gbs", 6650.0),
                               "frac": hbm_bytes / per_launch_s / 1e9 / peaks.get("hbm_gbs", 6650.0)}}
-        line["sinkhorn_cell_updates_per_s_fused_kernel"] = cell_updates / (ms_fused / 1e3)
+        line["sinkhorn_cell_updates_per_s_fused_kernel"] = cells_rank * T * a.steps / (ms_fused / 1e3) * world
 
     # e2e: the public API with host buffers, K outer steps, copies included
     if (world > 1 or a.sharded) and not a.no_e2e:
@@ -401,11 +467,12 @@ def run_ours(a):
 
 
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg1", choices=sorted(BASELINE_CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(BASELINE_CONFIGS))
     ap.add_argument("--dtype", default=None, choices=["float32", "float64"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -423,6 +490,10 @@ def main(argv=None):
     a.warmup = max(a.warmup, 3)
     if a.impl == "reference":
         return run_reference(a)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        rc = _spawn_ranks(a, argv)
+        if rc is not None:
+            return rc
     return run_ours(a)
 
 

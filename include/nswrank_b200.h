@@ -175,6 +175,11 @@ nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream);
 /* Device time (ms) of the last N fused step kernels, CUDA events. */
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused_kernel);
+/* Measurement helper for any shard (also world > 1): device time (ms, summed)
+ * of N replays of the fused step launch(es) alone, the L2 evicted before each;
+ * the state machine does not advance (no impact reduction / finalize), the
+ * iterate does.  Call at the end of a measurement. */
+nsw_status nsw_solver_time_fused(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_fused_kernel);
 /* Diagnostics: global-timer stamps (ns) of the fused kernel's phase
  * boundaries, [count users][16], of the last step the solver ran.  Only when
  * the environment had NSW_PHASE_TIMING=1 at nsw_solver_create. */
@@ -278,9 +283,13 @@ nsw_status nsw_cost_from_policy_f32(const float* plan, size_t count, double epsi
                                     void* stream);
 
 /* Page-locked host memory for results, from a small process-wide cache
- * (NULL on failure).  Free with nsw_host_free. */
+ * (at most 4 GiB of free blocks are kept; NULL on failure).  Free with
+ * nsw_host_free. */
 void* nsw_host_alloc(size_t bytes);
 void nsw_host_free(void* ptr);
+/* Return cached memory: the free page-locked host blocks, and the unused
+ * part of the solvers' private device pools (trimmed to zero). */
+void nsw_release_cached(void);
 
 /* Whether a (dtype, n, m, iters) problem has a compiled tile variant. */
 int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);

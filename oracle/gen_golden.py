@@ -266,11 +266,45 @@ def case_api():
     print(f"api: solve {st.iterations_used} iterations (converged {st.converged}), batch {rb.iterations}")
 
 
+def _long_job(args):
+    kind, users, outer = args
+    rel, expo, cfg = make_instance("cfg1", seed=0, user_slice=(0, users))
+    if kind == "ref":
+        return run_reference(rel, expo, cfg.epsilon, cfg.inner_iters, outer)
+    if kind == "perm":
+        perm = np.random.default_rng(123).permutation(rel.shape[1])
+        x, tr = run_reference(rel[:, perm], expo, cfg.epsilon, cfg.inner_iters, outer)
+        return x[:, np.argsort(perm), :], tr
+    return run_restatement(rel, expo, cfg.epsilon, cfg.inner_iters, outer)
+
+
+def case_cfg1_long(users=100, outer=200):
+    """the config-1 generator's first 100 users over 200
+    outer steps x 100 inner iterations (eps 0.05), the reference itself, its
+    item-permuted twin (the reference's own reorder noise floor) and the
+    restatement pin, run as three processes."""
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(3) as pool:
+        (x_ref, tr_ref), (x_perm, tr_perm), (x_or, tr_or) = pool.map(
+            _long_job, [("ref", users, outer), ("perm", users, outer), ("or", users, outer)])
+    pin("cfg1-100x200", x_ref, tr_ref, x_or, tr_or)
+    floor = float(np.abs(x_perm - x_ref).max())
+    floor_f = float(np.abs(np.array(tr_perm.objective) / np.array(tr_ref.objective) - 1).max())
+    print(f"[floor] cfg1 100x200 reorder noise floor max|dX| = {floor:.3e}, rel dF = {floor_f:.3e}")
+    rel, expo, cfg = make_instance("cfg1", seed=0, user_slice=(0, users))
+    np.savez(os.path.join(OUT, "cfg1_long.npz"), relevance=rel, exposure=expo,
+             policy_head=x_ref[:8], policy_checksums=checksums(x_ref),
+             objective=np.array(tr_ref.objective), grad_norm=np.array(tr_ref.grad_norm),
+             top_positions=orc.top_positions(x_ref), epsilon=cfg.epsilon, inner=cfg.inner_iters,
+             outer=outer, noise_floor=floor, noise_floor_objective=floor_f,
+             perm_objective=np.array(tr_perm.objective))
+
+
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
     which = sys.argv[1:] or ["ops", "cfg0", "tol", "cfg1", "metrics", "api"]
     for w in which:
         t = time.time()
         {"ops": case_ops, "cfg0": case_cfg0, "tol": case_tolerance_desk, "cfg1": case_cfg1_slice,
-         "metrics": case_metrics, "api": case_api}[w]()
+         "metrics": case_metrics, "api": case_api, "cfg1long": case_cfg1_long}[w]()
         print(f"  {w}: {time.time() - t:.1f}s")

@@ -10,7 +10,8 @@ __version__ = "0.1.0"
 
 _EXPORTS = {
     "core": ("ProblemShape", "RelevanceMatrix", "ExposureModel", "RankingPolicy", "SolverConfig",
-             "ShapeError", "DomainError", "StateError", "SolverError", "RELEVANCE_FLOOR", "uniform_policy"),
+             "ShapeError", "DomainError", "StateError", "SolverError", "RELEVANCE_FLOOR", "FEASIBILITY_TOL", "uniform_policy", "CostTensor",
+             "ValidationReport", "validate_policy"),
     "solver": ("SolveTrace", "DeviceOptions", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError",
                "impact", "nsw_objective", "nsw_gradient_wrt_policy", "AdamState", "adam_update"),
     "data": ("exposure_model", "make_instance", "BASELINE_CONFIGS"),
@@ -18,7 +19,7 @@ _EXPORTS = {
                  "sinkhorn_solve", "sinkhorn_backward", "cost_from_policy"),
     "ranking": ("top_positions",),
     "metrics": ("user_utility", "mean_max_envy", "items_better_off", "items_worse_off", "policy_metrics"),
-    "distributed": ("solve_fair_ranking_distributed", "shard_users"),
+    "distributed": ("solve_fair_ranking_distributed", "shard_users", "ShardedAscent"),
     "experiments": ("compute_policy", "install"),
 }
 

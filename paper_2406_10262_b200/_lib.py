@@ -68,13 +68,15 @@ SIGNATURES = {
     "nsw_solver_launch_count": (C.c_int64, [_vp]),
     "nsw_solver_variant": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "nsw_solver_tail_users": (_i32, [_vp]),
-    "nsw_solver_time_steps":(C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "nsw_solver_time_steps": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
+    "nsw_solver_time_fused": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float)]),
     "nsw_solver_phase_times": (C.c_int, [_vp, C.POINTER(C.c_uint64), _i32]),
     "nsw_solver_top_positions": (C.c_int, [_vp, C.POINTER(_i32)]),
     "nsw_solver_metrics": (C.c_int, [_vp, C.c_double, _dp]),
     "nsw_solver_flush_l2": (C.c_int, [_vp, _vp]),
     "nsw_host_alloc": (_vp, [C.c_size_t]),
     "nsw_host_free": (None, [_vp]),
+    "nsw_release_cached": (None, []),
     "nsw_solver_bind_tol_exchange": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_local": (C.c_int, [_vp, _vp]),
     "nsw_solver_tol_decide": (C.c_int, [_vp, _vp, C.POINTER(_i32)]),

@@ -48,6 +48,25 @@ nsw_status fail(nsw_status st, const std::string& msg) {
 
 constexpr size_t kMaxSmem = 227 * 1024;
 
+nsw_status pool_malloc(void** p, size_t bytes, cudaStream_t st);   // private device pool (below)
+
+// Every entry point that touches a solver runs on the solver's device and
+// gives the caller its current device back on return (a sharded caller's
+// rank r keeps its own device current).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (dev >= 0 && dev != prev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 int sizeof_dtype(int dt) { return dt == NSW_F64 ? 8 : 4; }
 
 // Pick the tile variant for (dtype, n, m, T): smallest M >= m, then the
@@ -109,6 +128,7 @@ const Variant* choose_wide_variant(const Variant* base, int n, int T) {
 
 struct nsw_solver {
   int dtype = 0;
+  int device = 0;                 // CUDA device the solver's memory and stream live on
   int U = 0, n = 0, m = 0, T = 0, outer_max = 0, world = 1;
   nsw_solver_config cfg{};
   nsw_device_options opt{};
@@ -215,7 +235,7 @@ nsw_status download_converted(int dtype, const void* src, double* dst, size_t co
   } else {
     // widen on the device, then one copy straight into the caller's buffer
     double* wide = nullptr;
-    CUDA_TRY(cudaMallocAsync((void**)&wide, count * 8 + 16, st));
+    if (nsw_status pe = pool_malloc((void**)&wide, count * 8 + 16, st); pe != NSW_OK) return pe;
     unsigned* bad = reinterpret_cast<unsigned*>(wide + count);   // one word past the values
     CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(unsigned), st));
     widen_kernel<<<sm_count() * 4, 256, 0, st>>>(static_cast<const float*>(src), wide, count, bad);
@@ -358,12 +378,44 @@ nsw_status read_state(nsw_solver* s) {
   return NSW_OK;
 }
 
+// Device memory of the solvers comes from a private stream-ordered pool per
+// device (created once, keeps its memory between solvers so a repeated solve
+// of the same size allocates without OS calls); the device's default pool,
+// which torch or other cudaMallocAsync users may share, is left untouched.
+// nsw_release_cached() trims it.
+std::mutex g_pool_mu;
+cudaMemPool_t g_pool[64] = {};
+
+cudaMemPool_t solver_pool(int device) {
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pool[device]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t p = nullptr;
+    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
+    g_pool[device] = p;
+  }
+  return g_pool[device];
+}
+
+nsw_status pool_malloc(void** p, size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  cudaMemPool_t pool = solver_pool(dev);
+  if (!pool) return fail(NSW_ERR_CUDA, "cudaMemPoolCreate failed");
+  CUDA_TRY(cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 16), pool, st));
+  return NSW_OK;
+}
+
 template <typename T>
 nsw_status dmalloc(T** p, size_t bytes, cudaStream_t st) {
-  // stream-ordered allocation from the device's default pool, which keeps
-  // its memory across solvers (release threshold raised once per device):
-  // a repeated solve of the same size allocates without OS calls
-  CUDA_TRY(cudaMallocAsync((void**)p, std::max<size_t>(bytes, 16), st));
+  nsw_status e = pool_malloc((void**)p, bytes, st);
+  if (e != NSW_OK) return e;
   CUDA_TRY(cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), st));
   return NSW_OK;
 }
@@ -398,18 +450,9 @@ void pinned_state_put(int* p) {
 std::mutex g_host_mu;
 std::multimap<size_t, void*> g_host_free;
 std::map<void*, size_t> g_host_size;
-constexpr size_t kHostCacheBlocks = 8;
+constexpr size_t kHostCacheBytes = size_t(4) << 30;   // cached (free) page-locked bytes at most
+size_t g_host_cached = 0;
 
-nsw_status keep_pool_memory(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return NSW_OK;
-  cudaMemPool_t pool;
-  CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t keep = ~uint64_t(0);
-  CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  done[device] = true;
-  return NSW_OK;
-}
 
 }  // namespace
 
@@ -423,6 +466,7 @@ void* nsw_host_alloc(size_t bytes) {
     auto it = g_host_free.find(bytes);
     if (it != g_host_free.end()) {
       void* p = it->second;
+      g_host_cached -= it->first;
       g_host_free.erase(it);
       return p;
     }
@@ -439,12 +483,32 @@ void nsw_host_free(void* p) {
   std::lock_guard<std::mutex> lk(g_host_mu);
   auto it = g_host_size.find(p);
   if (it == g_host_size.end()) return;
-  if (g_host_free.size() < kHostCacheBlocks) {
+  if (g_host_cached + it->second <= kHostCacheBytes) {
     g_host_free.emplace(it->second, p);
+    g_host_cached += it->second;
     return;
   }
   g_host_size.erase(it);
   cudaFreeHost(p);
+}
+
+void nsw_release_cached(void) {
+  {
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    for (auto& kv : g_host_free) {
+      g_host_size.erase(kv.second);
+      cudaFreeHost(kv.second);
+    }
+    g_host_free.clear();
+    g_host_cached = 0;
+  }
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  for (int d = 0; d < 64; ++d)
+    if (g_pool[d]) {
+      DeviceGuard guard(d);
+      cudaDeviceSynchronize();
+      cudaMemPoolTrimTo(g_pool[d], 0);
+    }
 }
 
 const char* nsw_version(void) { return "nswrank_b200 0.1.0 (sm_100a)"; }
@@ -489,7 +553,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +
                                          " n=" + std::to_string(n) + " m=" + std::to_string(m) +
                                          " T=" + std::to_string(T));
-  CUDA_TRY(cudaSetDevice(options->device));
+  // device < 0: the caller's current device
+  int dev = options->device;
+  if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
+  DeviceGuard guard(dev);
   // Cluster tiles: the GPU's GPC layout decides how many clusters of each size
   // can be resident (B200: 15 clusters of 8 or 9 CTAs, 7 of 16), so among the
   // tiles that hold n items pick the most users in flight per unit of per-user
@@ -528,13 +595,13 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     cudaGetLastError();   // a rejected candidate must not leave a sticky error behind
     if (best) var = best;
   }
-  if (nsw_status pe = keep_pool_memory(options->device); pe != NSW_OK) return pe;
   auto* s = new nsw_solver();
   if (cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking) != cudaSuccess) {
     delete s;
     return fail(NSW_ERR_CUDA, "cudaStreamCreate failed");
   }
   s->dtype = options->dtype;
+  s->device = dev;
   s->U = users_local;
   s->n = n;
   s->m = m;
@@ -543,6 +610,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   s->world = world;
   s->cfg = *config;
   s->opt = *options;
+  s->opt.device = dev;
   if (s->opt.check_every <= 0) s->opt.check_every = 8;
   s->var = var;
   s->smem = var->smem(T);
@@ -623,7 +691,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   s->U1 = users_local;
   if (options->variant == -1 && var->CL == 1) {
     int sms = 148, per_sm = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, options->device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // Fewer users than one wave of the throughput tile (e.g. a strong-scaling
     // shard): the tile with the fewest rows per thread (R >= 2) that still
     // holds every user in one wave has the shortest per-user latency
@@ -667,6 +735,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
       } else if (users_local > slots && rem > 0 && rem <= sms) {
         s->U1 = users_local - rem;
       }
+    }
+    // tests / experiments: force the main/tail split at user k (both tiles
+    // run, the tail on the side stream as in production)
+    if (const char* e = std::getenv("NSW_SPLIT_USERS"); e && wide && wide != var) {
+      const int k = std::atoi(e);
+      if (k >= 0 && k < users_local) s->U1 = k;
     }
     if (s->U1 < users_local) {
       s->var2 = wide;
@@ -744,6 +818,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
 
 nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (!s) return NSW_OK;
+  DeviceGuard guard(s->device);
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
@@ -766,6 +841,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
 
 nsw_status nsw_solver_exchange_buffers(nsw_solver* s, void** local_dev, void** gathered_dev) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   if (local_dev) *local_dev = s->imp_local;
   if (gathered_dev) *gathered_dev = s->imp_all;
   return NSW_OK;
@@ -773,6 +849,7 @@ nsw_status nsw_solver_exchange_buffers(nsw_solver* s, void** local_dev, void** g
 
 nsw_status nsw_solver_bind_exchange(nsw_solver* s, void* local_dev, void* gathered_dev) {
   if (!s || !local_dev || !gathered_dev) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   s->imp_local = (double*)local_dev;
   s->imp_all = (double*)gathered_dev;
   return refresh_args(s);
@@ -783,6 +860,7 @@ static nsw_status tol_decide(nsw_solver* s, cudaStream_t st, int* phase);
 
 nsw_status nsw_solver_bind_tol_exchange(nsw_solver* s, void* cmax_dev) {
   if (!s || !cmax_dev) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
   s->tolbuf = (double*)cmax_dev;
   return NSW_OK;
@@ -790,12 +868,14 @@ nsw_status nsw_solver_bind_tol_exchange(nsw_solver* s, void* cmax_dev) {
 
 nsw_status nsw_solver_tol_local(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
   return tol_local(s, stream ? (cudaStream_t)stream : s->stream);
 }
 
 nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
   int ph = 0;
   nsw_status e = tol_decide(s, stream ? (cudaStream_t)stream : s->stream, &ph);
@@ -805,11 +885,13 @@ nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
 
 nsw_status nsw_solver_local_step(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   return launch_step(s, stream ? (cudaStream_t)stream : s->stream);
 }
 
 nsw_status nsw_solver_finalize(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   return launch_finalize(s, stream ? (cudaStream_t)stream : s->stream);
 }
 
@@ -897,6 +979,7 @@ static nsw_status one_step(nsw_solver* s) {
 
 nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   if (s->world != 1) return fail(NSW_ERR_ARG, "nsw_solver_run drives a single shard (world == 1)");
   if (done) *done = 0;
   for (int it = 0; it < max_steps; ++it) {
@@ -917,6 +1000,7 @@ nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done) {
 
 nsw_status nsw_solver_status(nsw_solver* s, int32_t* phase, int32_t* steps, int32_t* errors) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   nsw_status e = read_state(s);
   if (e != NSW_OK) return e;
   if (phase) *phase = s->state_host[ST_PHASE];
@@ -927,12 +1011,14 @@ nsw_status nsw_solver_status(nsw_solver* s, int32_t* phase, int32_t* steps, int3
 
 nsw_status nsw_solver_stream(nsw_solver* s, void** stream) {
   if (!s || !stream) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   *stream = s->stream;
   return NSW_OK;
 }
 
 nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
   nsw_status e = read_state(s);
   if (e != NSW_OK) return e;
@@ -992,6 +1078,7 @@ static nsw_status field_ptr(nsw_solver* s, const char* f, void** p, size_t* coun
 
 nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t count) {
   if (!s || !field || !host) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   void* p;
   size_t c;
   bool typed;
@@ -1009,6 +1096,7 @@ nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t
 
 nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, size_t count) {
   if (!s || !field || !host) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   void* p;
   size_t c;
   bool typed;
@@ -1025,6 +1113,7 @@ nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, 
 
 nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value) {
   if (!s || !field) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
   int idx = -1;
   if (!strcmp(field, "phase")) idx = ST_PHASE;
@@ -1084,6 +1173,7 @@ static nsw_status launch_l2_flush(nsw_solver* s, cudaStream_t st) {
 
 nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  DeviceGuard guard(s->device);
   nsw_status e = ensure_flush_buffer(s);
   if (e != NSW_OK) return e;
   return launch_l2_flush(s, stream ? (cudaStream_t)stream : s->stream);
@@ -1092,6 +1182,7 @@ nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream) {
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,
                                  float* ms_fused) {
   if (!s || steps <= 0) return fail(NSW_ERR_ARG, "bad arguments");
+  DeviceGuard guard(s->device);
   if (s->world != 1) return fail(NSW_ERR_ARG, "timing helper drives a single shard");
   if (s->tol) return fail(NSW_ERR_ARG, "timing helper runs the fixed schedule");
   if (flush_l2) {
@@ -1156,8 +1247,61 @@ nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2,
   return NSW_OK;
 }
 
+// Measurement helper for any shard (world >= 1): device time of the fused
+// launch(es) alone -- no impact reduction, exchange or finalize, so the device
+// state machine does not advance; the iterate (C, Adam moments) does, without
+// a trace entry.  For timing at the end of a measurement only.
+nsw_status nsw_solver_time_fused(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_fused) {
+  if (!s || steps <= 0) return fail(NSW_ERR_ARG, "bad arguments");
+  DeviceGuard guard(s->device);
+  if (s->tol) return fail(NSW_ERR_ARG, "timing helper runs the fixed schedule");
+  if (flush_l2) {
+    nsw_status fe = ensure_flush_buffer(s);
+    if (fe != NSW_OK) return fe;
+  }
+  std::vector<cudaEvent_t> ev(size_t(2) * steps);
+  for (auto& x : ev) CUDA_TRY(cudaEventCreate(&x));
+  const int64_t before = s->launches;
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t gx = nullptr;
+  nsw_status e = NSW_OK;
+  if (cudaStreamBeginCapture(s->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    e = fail(NSW_ERR_CUDA, "graph capture");
+  } else {
+    e = launch_fused(s, s->stream);
+    cudaError_t ce = cudaStreamEndCapture(s->stream, &g);
+    if (e == NSW_OK && ce != cudaSuccess) e = fail(NSW_ERR_CUDA, "graph capture");
+    if (e == NSW_OK && cudaGraphInstantiate(&gx, g, 0) != cudaSuccess) e = fail(NSW_ERR_CUDA, "graph instantiate");
+    if (g) cudaGraphDestroy(g);
+  }
+  const int64_t per_step = s->launches - before;
+  s->launches = before;
+  for (int i = 0; i < steps && e == NSW_OK; ++i) {
+    if (flush_l2 && (e = launch_l2_flush(s, s->stream)) != NSW_OK) break;
+    if (cudaEventRecord(ev[2 * i], s->stream) != cudaSuccess || cudaGraphLaunch(gx, s->stream) != cudaSuccess ||
+        cudaEventRecord(ev[2 * i + 1], s->stream) != cudaSuccess) {
+      e = fail(NSW_ERR_CUDA, "timed launch failed");
+      break;
+    }
+    s->launches += per_step;
+  }
+  if (e == NSW_OK && cudaStreamSynchronize(s->stream) != cudaSuccess) e = fail(NSW_ERR_CUDA, "timed launches failed");
+  float tot = 0.f;
+  for (int i = 0; i < steps && e == NSW_OK; ++i) {
+    float a = 0.f;
+    cudaEventElapsedTime(&a, ev[2 * i], ev[2 * i + 1]);
+    tot += a;
+  }
+  if (gx) cudaGraphExecDestroy(gx);
+  for (auto& x : ev) cudaEventDestroy(x);
+  if (e != NSW_OK) return e;
+  if (ms_fused) *ms_fused = tot;
+  return NSW_OK;
+}
+
 nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host) {
   if (!s || !out_host) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   int32_t* d = nullptr;
   const size_t count = size_t(s->U) * (s->m - 1);
   CUDA_TRY(cudaMalloc(&d, count * sizeof(int32_t)));
@@ -1176,6 +1320,7 @@ nsw_status nsw_solver_top_positions(nsw_solver* s, int32_t* out_host) {
 
 nsw_status nsw_solver_metrics(nsw_solver* s, double threshold, double* out_host) {
   if (!s || !out_host) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   CUDA_TRY(cudaStreamSynchronize(s->stream));
   const nsw_status e =
       s->dtype == NSW_F64
@@ -1190,6 +1335,7 @@ nsw_status nsw_solver_metrics(nsw_solver* s, double threshold, double* out_host)
 
 nsw_status nsw_solver_phase_times(nsw_solver* s, uint64_t* out, int32_t count) {
   if (!s || !out) return fail(NSW_ERR_ARG, "NULL argument");
+  DeviceGuard guard(s->device);
   if (!s->phase_ns) return fail(NSW_ERR_UNSUPPORTED, "phase timing is off (set NSW_PHASE_TIMING=1 before creating the solver)");
   const size_t words = size_t(std::min(count, s->U)) * 16;
   CUDA_TRY(cudaStreamSynchronize(s->stream));

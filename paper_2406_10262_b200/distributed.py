@@ -23,6 +23,8 @@ step is host-driven (the number of chunks is data dependent), not captured.
 
 from __future__ import annotations
 
+import dataclasses
+
 import numpy as np
 
 from .core import ExposureModel, ProblemShape, RankingPolicy, RelevanceMatrix, SolverConfig, SolverError
@@ -69,7 +71,12 @@ class ShardedAscent:
         rsq_local = torch.tensor((rel[self.start:self.stop] ** 2).sum(axis=0), dtype=torch.float64, device=dev)
         dist.all_reduce(rsq_local, group=group)
         rsq = rsq_local.cpu().numpy()
-        opts = options or DeviceOptions(schedule="fixed")
+        # the drop-in's defaults (reference tolerance schedule, float64), on
+        # this rank's current device
+        opts = options or DeviceOptions()
+        if opts.device is None:
+            opts = dataclasses.replace(opts, device=dev.index)
+        self.device = dev
         self.tolerance = opts.schedule == "tolerance"
         self.solver = DeviceSolver(rel[self.start:self.stop], exposure.values, shape.num_items,
                                    shape.num_positions, config, opts, rel_sq_sum=rsq, world=self.world)
@@ -141,23 +148,42 @@ class ShardedAscent:
 
 
 def solve_fair_ranking_distributed(relevance, exposure, shape, config, options: DeviceOptions | None = None,
-                                   group=None, gather_policy=True):
-    """SPMD drop-in: every rank calls it with the full inputs; each solves its
-    user block.  Returns (RankingPolicy of the full instance on every rank if
-    ``gather_policy`` else this rank's block, SolveTrace)."""
+                                   group=None, gather_policy=False):
+    """SPMD drop-in: every rank calls it with the full inputs and the same
+    arguments as ``solve_fair_ranking`` (same defaults: the reference's
+    tolerance schedule in float64); each rank solves its user block on its
+    current CUDA device.
+
+    Returns (RankingPolicy, SolveTrace).  The policy is this rank's user block
+    [start, stop) (``gather_policy=False``, default: at config 4 the full
+    float64 policy is 163 GB), or, with ``gather_policy=True``, the full
+    [U][n][m] policy assembled on every rank by one device all-gather (NCCL)
+    of the equal-size padded blocks -- for instances whose full policy fits
+    host memory."""
     import torch
 
     relevance, exposure, shape, config = _coerce(relevance, exposure, shape, config)
     _check_instance(relevance.values, exposure.values, shape)
+    options = options or DeviceOptions()
     sa = ShardedAscent(relevance, exposure, shape, config, options, group)
-    done = sa.run(config.outer_max_iters + 1, use_graph=bool((options or DeviceOptions(schedule="fixed")).use_graph))
-    torch.cuda.synchronize()
-    if not done:
-        raise SolverError("distributed solve did not reach its stop state")
-    pol, trace = sa.solver.result()
-    sa.solver.close()
+    try:
+        done = sa.run(config.outer_max_iters + 1, use_graph=bool(options.use_graph))
+        torch.cuda.synchronize()
+        if not done:
+            raise SolverError("distributed solve did not reach its stop state")
+        pol, trace = sa.solver.result()
+    finally:
+        sa.solver.close()
     if not gather_policy:
         return RankingPolicy(pol), trace
-    parts = [None] * sa.world
-    sa.dist.all_gather_object(parts, pol, group=group)
-    return RankingPolicy(np.concatenate(parts, axis=0)), trace
+    U, n, m = shape.num_users, shape.num_items, shape.num_positions
+    per = -(-U // sa.world)
+    block = torch.zeros((per, n, m), dtype=torch.float64, device=sa.device)
+    block[: sa.stop - sa.start].copy_(torch.from_numpy(np.ascontiguousarray(pol)))
+    full = torch.empty((sa.world * per, n, m), dtype=torch.float64, device=sa.device)
+    sa.dist.all_gather_into_tensor(full, block, group=group)
+    parts = []
+    for r in range(sa.world):
+        s0, s1 = shard_users(U, sa.world, r)
+        parts.append(full[r * per: r * per + (s1 - s0)])
+    return RankingPolicy(torch.cat(parts).cpu().numpy()), trace

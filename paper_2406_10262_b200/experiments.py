@@ -39,10 +39,15 @@ def compute_policy(method, rel, exposure, shape, solver_cfg, options: DeviceOpti
 
 
 def install(experiments_module, options: DeviceOptions | None = None):
-    """Register the device method in a loaded ``nswrank.experiments`` module:
-    ``METHODS`` gains ``"nsw_algo1_b200"`` (so INI configs may name it) and
-    ``_compute_policy`` dispatches it to the device, every other method to the
-    reference's original function.  Returns the module."""
+    """Register the device method in a loaded ``nswrank.experiments`` module.
+
+    ``_compute_policy`` dispatches ``"nsw_algo1_b200"`` to the device and every
+    other method to the reference's original function; ``_methods``
+    (experiments.py:88-96) additionally ACCEPTS the device method when a
+    config names it.  ``METHODS`` -- and so the default method list of a
+    config without a [methods] section -- is left unchanged: such configs
+    keep running exactly the reference's methods (and need no GPU).
+    Returns the module."""
     original = experiments_module._compute_policy
     if getattr(original, "_nsw_b200", False):
         return experiments_module
@@ -52,6 +57,22 @@ def install(experiments_module, options: DeviceOptions | None = None):
 
     _compute_policy._nsw_b200 = True
     experiments_module._compute_policy = _compute_policy
-    if METHOD not in tuple(experiments_module.METHODS):
-        experiments_module.METHODS = tuple(experiments_module.METHODS) + (METHOD,)
+    original_methods = getattr(experiments_module, "_methods", None)
+    if original_methods is not None:
+        def _methods(cfg):
+            mod = experiments_module
+            default = ", ".join(mod.METHODS)
+            raw = mod._get(cfg, "methods", "methods", str, default) if hasattr(mod, "_get") else default
+            names = [tok.strip() for tok in raw.split(",") if tok.strip()]
+            if METHOD not in names:
+                return original_methods(cfg)       # the reference's own validation and messages
+            allowed = tuple(mod.METHODS) + (METHOD,)
+            err = getattr(mod, "ConfigError", ConfigError)
+            for name in names:
+                if name not in allowed:
+                    raise err(f"unknown method {name!r}, expected one of {allowed}")
+            return names
+
+        _methods._nsw_b200 = True
+        experiments_module._methods = _methods
     return experiments_module

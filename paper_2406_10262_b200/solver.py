@@ -58,7 +58,9 @@ class DeviceOptions:
               exactly ``config.sinkhorn_max_iters`` iterations (the reference
               with the fixed-schedule shim; what BASELINE.json
               measures).
-    device    CUDA device ordinal.
+    device    CUDA device ordinal; None (default) = the caller's current
+              device.  The library runs every call on the solver's device and
+              restores the caller's current device before returning.
     variant   -1 = automatic tile choice; >= 0 forces a compiled tile shape.
     use_graph capture the outer step in a CUDA graph (fixed schedule).
     check_every  poll the device stop flag every N outer steps.
@@ -67,7 +69,7 @@ class DeviceOptions:
 
     dtype: str = "float64"
     schedule: str = "tolerance"
-    device: int = 0
+    device: int | None = None
     variant: int = -1
     use_graph: bool = True
     check_every: int = 16
@@ -81,7 +83,7 @@ class DeviceOptions:
         return _lib.DeviceOptionsC(
             _lib.NSW_F64 if self.dtype == "float64" else _lib.NSW_F32,
             _lib.NSW_SCHEDULE_FIXED if self.schedule == "fixed" else _lib.NSW_SCHEDULE_TOLERANCE,
-            int(self.device), int(self.variant), int(bool(self.use_graph)), int(self.check_every),
+            -1 if self.device is None else int(self.device), int(self.variant), int(bool(self.use_graph)), int(self.check_every),
             int(self.tol_chunk))
 
 
@@ -246,6 +248,13 @@ class DeviceSolver:
         tot, fus = C.c_float(), C.c_float()
         check(self.lib.nsw_solver_time_steps(self.h, int(steps), int(flush_l2), C.byref(tot), C.byref(fus)))
         return tot.value, fus.value
+
+    def time_fused(self, steps: int, flush_l2: bool = True) -> float:
+        """Device ms of ``steps`` replays of the fused launch(es) alone (any
+        world size; advances the iterate without a trace entry: call last)."""
+        ms = C.c_float()
+        check(self.lib.nsw_solver_time_fused(self.h, int(steps), int(flush_l2), C.byref(ms)), "time_fused")
+        return ms.value
 
     def phase_times(self) -> np.ndarray:
         """Diagnostics: [U][16] global-timer stamps (ns) of the fused kernel's

@@ -18,13 +18,13 @@ def test_unknown_method_raises():
     assert ex.METHODS[:4] == ex.REFERENCE_METHODS and ex.METHOD in ex.METHODS
 
 
-def test_install_extends_methods_and_delegates():
+def test_install_keeps_methods_and_delegates():
     calls = []
     fake = types.SimpleNamespace(METHODS=ex.REFERENCE_METHODS,
                                  _compute_policy=lambda *a: calls.append(a[0]) or "ref")
     ex.install(fake)
     ex.install(fake)   # idempotent
-    assert fake.METHODS.count(ex.METHOD) == 1
+    assert fake.METHODS == ex.REFERENCE_METHODS   # the default method list is unchanged
     assert fake._compute_policy("uniform", 1, 2, 3, 4) == "ref" and calls == ["uniform"]
 
 
@@ -37,15 +37,26 @@ def test_install_into_reference_runner():
         import importlib
         rexp = importlib.import_module("nswrank.experiments")
         core = importlib.import_module("nswrank.core")
-        saved = (rexp.METHODS, rexp._compute_policy)
+        saved = (rexp.METHODS, rexp._compute_policy, rexp._methods)
         try:
             ex.install(rexp)
-            assert ex.METHOD in rexp.METHODS
+            assert ex.METHOD not in rexp.METHODS
+            # a config without [methods] keeps the reference default list
+            import configparser
+            cfg = configparser.ConfigParser()
+            assert rexp._methods(cfg) == list(ex.REFERENCE_METHODS)
+            # a config naming the device method is accepted; unknown names still fail
+            cfg.read_string("[methods]\nmethods = uniform, nsw_algo1_b200\n")
+            assert rexp._methods(cfg) == ["uniform", ex.METHOD]
+            bad = configparser.ConfigParser()
+            bad.read_string("[methods]\nmethods = uniform, nope\n")
+            with pytest.raises(rexp.ConfigError):
+                rexp._methods(bad)
             shape = core.ProblemShape(3, 5, 3)
             pol = rexp._compute_policy("uniform", None, None, shape, None)
             assert pol.values.shape == (3, 5, 3)
         finally:
-            rexp.METHODS, rexp._compute_policy = saved
+            rexp.METHODS, rexp._compute_policy, rexp._methods = saved
     finally:
         sys.path.remove(REF_SRC)
 
