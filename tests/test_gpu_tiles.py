@@ -55,14 +55,24 @@ def check_one_step(name, rel, expo, eps, T, step=3):
     r32 = orc.one_step(rel, expo, st, p, dtype=np.float32)
     dev = resume_one_step(rel, expo, p, st, step)
     dx = float(np.abs(dev["plan"] - ref["plan"]).max())
-    dc = float(np.abs(dev["cost"] - ref["cost"]).max())
     dx32 = float(np.abs(r32["plan"].astype(np.float64) - ref["plan"]).max())
-    dc32 = float(np.abs(r32["cost"].astype(np.float64) - ref["cost"]).max())
+    # C_{t+1}: Adam's step m^/(sqrt(v^) + 1e-8) is scale-free, so cells whose
+    # gradient lies below fp32 resolution relative to the tile's largest
+    # (|g| < 1e-6 max|g|, e.g. plans of 1e-80 at eps = 0.01) take an O(lr)
+    # step of arbitrary sign in ANY fp32 arithmetic; C parity is
+    # judged on the resolvable cells, and every cell must stay within 1e-3
+    g = ref["grad_cost"]
+    ok = np.abs(g) >= 1e-6 * np.abs(g).max()
+    dcell = np.abs(dev["cost"] - ref["cost"])
+    dc = float(dcell[ok].max())
+    dc32 = float(np.abs(r32["cost"].astype(np.float64) - ref["cost"])[ok].max())
     df = abs(dev["objective"] / st["objective"] - 1)
     print(f"{name} {dev['variant']}: |dX|={dx:.2e} (fp32 oracle {dx32:.2e}) |dC|={dc:.2e} "
-          f"(fp32 oracle {dc32:.2e}) rel dF={df:.2e}")
+          f"(fp32 oracle {dc32:.2e}; {int((~ok).sum())} unresolvable cells, worst {dcell.max():.1e}) "
+          f"rel dF={df:.2e}")
     assert dx <= max(2e-6, 2 * dx32), (dx, dx32)
     assert dc <= max(5e-6, 2 * dc32), (dc, dc32)
+    assert (dcell > 1e-3).sum() == 0
     assert df <= 1e-6
     return dev["variant"]
 
@@ -71,20 +81,23 @@ def check_one_step(name, rel, expo, eps, T, step=3):
 PRODUCTION = [
     ("cfg1", 12, 30, "8,64,6", 6, (11, 8, 64), (2, 256)),     # bench cfg1: main wave + concurrent tail
     ("cfg2", 6, 30, "4,256,1", 3, (21, 4, 256), (2, 512)),    # bench cfg2 main tile + its tail
-    ("cfg3", 4, 30, "8,256,1", 2, (11, 8, 256), None),        # cfg3 main tile (+ its wide tail)
+    ("cfg3", 4, 30, "8,256,1", None, (11, 8, 256), None),     # cfg3 main tile (2048 rows: it is its own wide tile)
 ]
 
 
 @pytest.mark.parametrize("name,users,T,main,split,want,tail", PRODUCTION)
 def test_production_tile_one_step(monkeypatch, name, users, T, main, split, want, tail):
     monkeypatch.setenv("NSW_MAIN_TILE", main)
-    monkeypatch.setenv("NSW_SPLIT_USERS", str(split))
+    if split is not None:
+        monkeypatch.setenv("NSW_SPLIT_USERS", str(split))
     rel, expo, cfg = make_instance(name, seed=0, user_slice=(0, users))
     v = check_one_step(name, rel, expo, cfg.epsilon, T)
     assert (v["M"], v["R"], v["NT"]) == want
-    assert v.get("tail_users") == users - split
     if tail is not None:
+        assert v.get("tail_users") == users - split
         assert (v["tail_R"], v["tail_NT"]) == tail
+    else:
+        assert "tail_users" not in v
 
 
 def test_cfg1_natural_tile_choice_one_step():
