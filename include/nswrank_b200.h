@@ -291,8 +291,13 @@ void nsw_host_free(void* ptr);
  * part of the solvers' private device pools (trimmed to zero). */
 void nsw_release_cached(void);
 
-/* Whether a (dtype, n, m, iters) problem has a compiled tile variant. */
+/* Whether a (dtype, n, m, iters) problem runs on the device: every shape the
+ * reference accepts (2 <= m <= n, reference core.py:60-66) does. */
 int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);
+/* Whether it runs on a compiled on-chip tile (register / shared-memory /
+ * cluster resident); otherwise the streaming fused step (K~ and the adjoint
+ * in an L2-resident per-CTA scratch) runs it. */
+int32_t nsw_tiled(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);
 
 #ifdef __cplusplus
 }

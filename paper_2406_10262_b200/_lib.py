@@ -49,6 +49,7 @@ SIGNATURES = {
     "nsw_last_error": (C.c_char_p, []),
     "nsw_version": (C.c_char_p, []),
     "nsw_supported": (_i32, [_i32, _i32, _i32, _i32]),
+    "nsw_tiled": (_i32, [_i32, _i32, _i32, _i32]),
     "nsw_solve_fair_ranking": (C.c_int, [_dp, _dp, _i32, _i32, _i32, C.POINTER(SolverConfigC),
                                          C.POINTER(DeviceOptionsC), _dp, C.POINTER(TraceC)]),
     "nsw_solver_create": (C.c_int, [_dp, _dp, _i32, _i32, _i32, _dp, _i32, C.POINTER(SolverConfigC),

@@ -30,7 +30,8 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
 # (f64?, M) instantiations of the fused step kernel; any m <= 32 pads up.
 INSTANCES = [(f64, M) for f64 in (0, 1) for M in (4, 8, 11, 16, 21, 32)]
 
-HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_registry.h"]
+HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_registry.h", "nsw_step_generic.cuh",
+           "nsw_generic.h"]
 
 
 def _nvcc():
@@ -54,7 +55,7 @@ def _jobs(build_dir=BUILD):
     for f64 in (0, 1):
         jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(build_dir, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
                      [f"-DNSW_F64={f64}"]))
-    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics"):
+    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics", "nsw_generic"):
         jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(build_dir, name + ".o"), []))
     return jobs
 

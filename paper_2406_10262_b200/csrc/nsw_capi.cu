@@ -18,6 +18,7 @@
 #include <vector>
 
 #include "../../include/nswrank_b200.h"
+#include "nsw_generic.h"
 #include "nsw_registry.h"
 #include "nsw_step_kernel.cuh"
 
@@ -132,7 +133,10 @@ struct nsw_solver {
   int U = 0, n = 0, m = 0, T = 0, outer_max = 0, world = 1;
   nsw_solver_config cfg{};
   nsw_device_options opt{};
-  const Variant* var = nullptr;   // tile of the main launch (users [0, U1))
+  const Variant* var = nullptr;   // tile of the main launch (users [0, U1)); nullptr: streaming path
+  bool generic = false;           // streaming fused step (no on-chip tile holds the user)
+  int gen_ctas = 0;               // its CTAs (persistent over users)
+  void* gen_scratch = nullptr;    // [gen_ctas][gen_scratch_elems] K~ / adjoint / row + column vectors
   size_t smem = 0;
   const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
   size_t smem2 = 0;
@@ -270,6 +274,14 @@ nsw_status validate_config(const nsw_solver_config* c) {
 nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   void* args32[] = {&s->a32};
   void* args64[] = {&s->a64};
+  if (s->generic) {
+    const cudaError_t ce = s->dtype == NSW_F64
+                               ? gen_launch(s->a64, static_cast<double*>(s->gen_scratch), s->gen_ctas, st)
+                               : gen_launch(s->a32, static_cast<float*>(s->gen_scratch), s->gen_ctas, st);
+    if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("streaming step launch: ") + cudaGetErrorString(ce));
+    s->launches += 1;
+    return NSW_OK;
+  }
   if (s->var->CL > 1) {
     // thread-block cluster of CL CTAs per user (DSMEM column reductions)
     cudaLaunchConfig_t lc = {};
@@ -514,6 +526,13 @@ void nsw_release_cached(void) {
 const char* nsw_version(void) { return "nswrank_b200 0.1.0 (sm_100a)"; }
 
 int32_t nsw_supported(int32_t dtype, int32_t n, int32_t m, int32_t iters) {
+  // every shape the reference accepts (2 <= m <= n, core.py:60-66): an
+  // on-chip tile when one holds it, else the streaming fused step
+  if ((dtype != NSW_F32 && dtype != NSW_F64) || m < 2 || m > n || iters <= 0) return 0;
+  return 1;
+}
+
+int32_t nsw_tiled(int32_t dtype, int32_t n, int32_t m, int32_t iters) {
   return choose_variant(dtype, n, m, iters, -1) != nullptr;
 }
 
@@ -549,10 +568,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
             v.CL * v.rows >= n)
           var = &v;
   }
-  if (!var)
-    return fail(NSW_ERR_UNSUPPORTED, "no compiled tile variant for dtype=" + std::to_string(options->dtype) +
-                                         " n=" + std::to_string(n) + " m=" + std::to_string(m) +
-                                         " T=" + std::to_string(T));
+  // no on-chip tile holds the user's n x m tile (or forced with variant -3):
+  // the streaming fused step, any shape
+  const bool generic = !var || options->variant == -3;
+  if (generic) var = nullptr;
   // device < 0: the caller's current device
   int dev = options->device;
   if (dev < 0) CUDA_TRY(cudaGetDevice(&dev));
@@ -613,7 +632,8 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   s->opt.device = dev;
   if (s->opt.check_every <= 0) s->opt.check_every = 8;
   s->var = var;
-  s->smem = var->smem(T);
+  s->generic = generic;
+  s->smem = generic ? 0 : var->smem(T);
   const size_t es = sizeof_dtype(s->dtype);
   const size_t cells = size_t(users_local) * n * m;
   nsw_status e = NSW_OK;
@@ -653,6 +673,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->counter, 16);
   ALLOC(s->state, ST_WORDS * sizeof(int));
   ALLOC(s->iters, size_t(s->outer_max) * sizeof(int));
+  if (generic) {
+    s->gen_ctas = gen_ctas(s->dtype, users_local);
+    ALLOC(s->gen_scratch, size_t(s->gen_ctas) * gen_scratch_elems(n, m) * es);
+  }
   if (const char* pt = std::getenv("NSW_PHASE_TIMING"); pt && *pt && *pt != '0') {
     ALLOC(s->phase_ns, size_t(users_local) * 16 * 8);
     CUDA_TRY(cudaMemset(s->phase_ns, 0, size_t(users_local) * 16 * 8));
@@ -678,18 +702,20 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaMallocHost failed");
   }
-  if (var->CL > 8 && cudaFuncSetAttribute(var->fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+  if (!generic && var->CL > 8 &&
+      cudaFuncSetAttribute(var->fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_UNSUPPORTED, "16-CTA clusters are not available on this device");
   }
-  if (cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) != cudaSuccess) {
+  if (!generic && cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) !=
+                      cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");
   }
   // Wave split: whole waves of the main tile, then (if what is left is at
   // most one user per SM) a tail launch with the wide tile.
   s->U1 = users_local;
-  if (options->variant == -1 && var->CL == 1) {
+  if (!generic && options->variant == -1 && var->CL == 1) {
     int sms = 148, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // Fewer users than one wave of the throughput tile (e.g. a strong-scaling
@@ -823,7 +849,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
                   s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->res, s->iters,
-                  s->phase_ns, s->own_tol};
+                  s->phase_ns, s->own_tol, s->gen_scratch};
   if (s->stream) {
     for (void* p : bufs)
       if (p) cudaFreeAsync(p, s->stream);   // back to the pool, stream-ordered
@@ -1143,6 +1169,13 @@ nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
   // main tile; when a tail launch exists its shape is reported in the upper
   // 16 bits of R and NT (R | R2 << 16, NT | NT2 << 16) and *smem is the main one
+  if (s->generic) {   // streaming path: M = 0, R = CTAs of the launch
+    if (M) *M = 0;
+    if (R) *R = s->gen_ctas;
+    if (NT) *NT = GEN_NT;
+    if (smem) *smem = 0;
+    return NSW_OK;
+  }
   if (M) *M = s->var->M;
   if (R) *R = s->var->R | (s->var2 && s->U1 < s->U ? s->var2->R << 16 : 0);
   if (NT) *NT = s->var->NT | (s->var2 && s->U1 < s->U ? s->var2->NT << 16 : 0);

@@ -61,7 +61,9 @@ class DeviceOptions:
     device    CUDA device ordinal; None (default) = the caller's current
               device.  The library runs every call on the solver's device and
               restores the caller's current device before returning.
-    variant   -1 = automatic tile choice; >= 0 forces a compiled tile shape.
+    variant   -1 = automatic tile choice; >= 0 forces a compiled tile shape;
+              -3 forces the streaming fused step (any shape; what runs when
+              no on-chip tile holds the user's n x m tile).
     use_graph capture the outer step in a CUDA graph (fixed schedule).
     check_every  poll the device stop flag every N outer steps.
     tol_chunk inner iterations per forward launch in the tolerance schedule.
@@ -231,6 +233,8 @@ class DeviceSolver:
     def variant(self):
         M, R, NT, sm = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
         check(self.lib.nsw_solver_variant(self.h, C.byref(M), C.byref(R), C.byref(NT), C.byref(sm)))
+        if M.value == 0:   # streaming fused step (no on-chip tile holds the user)
+            return dict(M=0, generic=True, ctas=R.value, NT=NT.value, smem=0)
         out = dict(M=M.value, R=R.value & 0xFFFF, NT=NT.value & 0xFFFF, smem=sm.value)
         tail = int(self.lib.nsw_solver_tail_users(self.h))
         if tail > 0:

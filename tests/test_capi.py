@@ -44,13 +44,22 @@ def test_library_is_sm100a_only():
                                           (1, 2048, 11, 100), (1, 2000, 51, 500), (0, 4000, 51, 500)])
 def test_supported_variants(dtype, n, m, T):
     assert _lib.load().nsw_supported(dtype, n, m, T) == 1
+    assert _lib.load().nsw_tiled(dtype, n, m, T) == 1
 
 
-def test_unsupported_shapes_reported():
+def test_every_reference_shape_supported_tiles_where_they_fit():
+    """Every shape the reference accepts runs (core.py:60-66: 2 <= m <= n);
+    shapes no on-chip tile holds run on the streaming fused step."""
     lib = _lib.load()
-    assert lib.nsw_supported(0, 100, 60, 10) == 0    # m > 52: no tile yet
-    assert lib.nsw_supported(0, 9000, 11, 10) == 0   # n > 8192 (16 CTAs x 512 items)
-    assert lib.nsw_supported(1, 4000, 11, 10) == 0   # float64 beyond 2048 items
+    assert lib.nsw_supported(1, 4000, 51, 200) == 1     # config 4 in float64
+    assert lib.nsw_supported(0, 100, 60, 10) == 1       # m > 52
+    assert lib.nsw_supported(0, 9000, 11, 10) == 1      # n > 8192
+    assert lib.nsw_supported(0, 5, 6, 10) == 0          # m > n: rejected like the reference
+    assert lib.nsw_supported(0, 5, 1, 10) == 0          # m < 2
+    assert lib.nsw_tiled(0, 100, 60, 10) == 0           # m > 52: no tile yet
+    assert lib.nsw_tiled(0, 9000, 11, 10) == 0          # n > 8192 (16 CTAs x 512 items)
+    assert lib.nsw_tiled(1, 4000, 11, 10) == 0          # float64 beyond 2048 items
+    assert lib.nsw_tiled(0, 4000, 51, 200) == 1
 
 
 def _create(rel, expo, n, m, cfg, opt):
