@@ -50,6 +50,7 @@ nsw_status fail(nsw_status st, const std::string& msg) {
 constexpr size_t kMaxSmem = 227 * 1024;
 
 nsw_status pool_malloc(void** p, size_t bytes, cudaStream_t st);   // private device pool (below)
+void pool_free(void* p, cudaStream_t st);
 
 // Every entry point that touches a solver runs on the solver's device and
 // gives the caller its current device back on return (a sharded caller's
@@ -247,7 +248,7 @@ nsw_status download_converted(int dtype, const void* src, double* dst, size_t co
     unsigned bad_h = 0;
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(dst, wide, count * 8, cudaMemcpyDeviceToHost, st);
     if (ce == cudaSuccess) ce = cudaMemcpyAsync(&bad_h, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
-    cudaFreeAsync(wide, st);
+    pool_free(wide, st);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
     if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("download: ") + cudaGetErrorString(ce));
     if (nonfinite) *nonfinite = bad_h != 0;
@@ -415,13 +416,84 @@ cudaMemPool_t solver_pool(int device) {
   return g_pool[device];
 }
 
+#if NSW_CHECKS
+// checked builds: 64 KB canary bands on both sides of every solver buffer,
+// verified when the buffer is freed (an out-of-bounds write aborts loudly)
+constexpr size_t kGuard = size_t(64) << 10;
+std::mutex g_guard_mu;
+std::map<void*, std::pair<void*, size_t>> g_guarded;   // user pointer -> (base, bytes)
+#endif
+
 nsw_status pool_malloc(void** p, size_t bytes, cudaStream_t st) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   cudaMemPool_t pool = solver_pool(dev);
   if (!pool) return fail(NSW_ERR_CUDA, "cudaMemPoolCreate failed");
-  CUDA_TRY(cudaMallocFromPoolAsync(p, std::max<size_t>(bytes, 16), pool, st));
+  bytes = std::max<size_t>(bytes, 16);
+#if NSW_CHECKS
+  void* base = nullptr;
+  CUDA_TRY(cudaMallocFromPoolAsync(&base, bytes + 2 * kGuard, pool, st));
+  CUDA_TRY(cudaMemsetAsync(base, 0xA5, kGuard, st));
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(base) + kGuard + bytes, 0xA5, kGuard, st));
+  *p = static_cast<char*>(base) + kGuard;
+  std::lock_guard<std::mutex> lk(g_guard_mu);
+  g_guarded[*p] = {base, bytes};
+#else
+  CUDA_TRY(cudaMallocFromPoolAsync(p, bytes, pool, st));
+#endif
   return NSW_OK;
+}
+
+void pool_free(void* p, cudaStream_t st) {
+  if (!p) return;
+#if NSW_CHECKS
+  std::pair<void*, size_t> e{nullptr, 0};
+  {
+    std::lock_guard<std::mutex> lk(g_guard_mu);
+    auto it = g_guarded.find(p);
+    if (it != g_guarded.end()) {
+      e = it->second;
+      g_guarded.erase(it);
+    }
+  }
+  if (!e.first) {
+    cudaFreeAsync(p, st);
+    return;
+  }
+  std::vector<unsigned char> lo(kGuard), hi(kGuard);
+  cudaError_t ce = cudaStreamSynchronize(st);
+  if (ce == cudaSuccess) ce = cudaMemcpy(lo.data(), e.first, kGuard, cudaMemcpyDeviceToHost);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpy(hi.data(), static_cast<char*>(e.first) + kGuard + e.second, kGuard, cudaMemcpyDeviceToHost);
+  if (ce != cudaSuccess) {   // a dead context (e.g. a trapped kernel) cannot be checked
+    std::fprintf(stderr, "NSW_CHECKS: guard bands not verifiable: %s\n", cudaGetErrorString(ce));
+    return;
+  }
+  size_t bad_lo = 0, bad_hi = 0, first_lo = kGuard, last_lo = 0, first_hi = kGuard, last_hi = 0;
+  for (size_t i = 0; i < kGuard; ++i) {
+    if (lo[i] != 0xA5) {
+      ++bad_lo;
+      first_lo = std::min(first_lo, i);
+      last_lo = i;
+    }
+    if (hi[i] != 0xA5) {
+      ++bad_hi;
+      first_hi = std::min(first_hi, i);
+      last_hi = i;
+    }
+  }
+  if (bad_lo || bad_hi) {
+    std::fprintf(stderr,
+                 "NSW_CHECKS: guard bands of a %zu-byte solver buffer at %p overwritten: low %zu bytes "
+                 "[%zu, %zu] (offsets from 64 KB below the buffer), high %zu bytes [%zu, %zu]\n",
+                 e.second, p, bad_lo, first_lo, last_lo, bad_hi, first_hi, last_hi);
+    std::fflush(stderr);
+    std::abort();
+  }
+  cudaFreeAsync(e.first, st);
+#else
+  cudaFreeAsync(p, st);
+#endif
 }
 
 template <typename T>
@@ -852,7 +924,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
                   s->phase_ns, s->own_tol, s->gen_scratch};
   if (s->stream) {
     for (void* p : bufs)
-      if (p) cudaFreeAsync(p, s->stream);   // back to the pool, stream-ordered
+      if (p) pool_free(p, s->stream);   // back to the pool, stream-ordered
     cudaStreamSynchronize(s->stream);
   }
   if (s->flush_buf) cudaFree(s->flush_buf);

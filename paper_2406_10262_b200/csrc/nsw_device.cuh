@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <type_traits>
 
@@ -47,6 +48,52 @@ enum : int {
 enum : int { ST_PHASE = 0, ST_STEP = 1, ST_IMPROVED = 2, ST_ERR = 3, ST_T0 = 4, ST_TSTAR = 5, ST_CONV = 6 };
 constexpr int ST_WORDS = 8;
 enum : int { ERR_IMPACT = 1, ERR_NONFINITE = 2, ERR_SOLVER = 4 };
+
+// ---------------------------------------------------------------------------
+// Checked build (-DNSW_CHECKS=1, `build.py --tag checked -D NSW_CHECKS=1`):
+// the tests run against it in place of compute-sanitizer (closed on the GPU
+// pool).  Every vector shared-memory access of the tiles is bounds-checked
+// against the CTA's shared-memory size, the dynamic shared memory is poisoned
+// with NaN at kernel entry (a read of a never-written slot propagates NaN into
+// the parity comparisons), mbarrier waits trap after ~2^28 polls instead of
+// hanging, and every solver buffer gets 64 KB canary guard bands that are
+// verified when it is freed (nsw_capi.cu).
+// ---------------------------------------------------------------------------
+#ifndef NSW_CHECKS
+#define NSW_CHECKS 0
+#endif
+
+__device__ __forceinline__ void nsw_check_fail(const char* what, unsigned a, unsigned b) {
+  printf("NSW_CHECKS: %s (block %d thread %d: %u vs %u)\n", what, int(blockIdx.x), int(threadIdx.x), a, b);
+  __trap();
+}
+
+// shared-memory window [p, p + bytes) lies inside this CTA's shared memory
+__device__ __forceinline__ void nsw_check_smem(const void* p, unsigned bytes) {
+  if constexpr (NSW_CHECKS) {
+    if (!__isShared(p)) nsw_check_fail("vector access outside shared memory", 0u, 0u);
+    unsigned total, dyn;
+    asm("mov.u32 %0, %%total_smem_size;" : "=r"(total));
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    extern __shared__ __align__(16) unsigned char nsw_dyn_base[];
+    // the dynamic window [base, base + dyn) ends the CTA's shared memory
+    const unsigned base = static_cast<unsigned>(__cvta_generic_to_shared(nsw_dyn_base));
+    const unsigned off = static_cast<unsigned>(__cvta_generic_to_shared(p));
+    if (off + bytes > base + dyn)
+      nsw_check_fail("shared-memory access past the CTA's allocation", off + bytes - base, dyn);
+    (void)total;
+  }
+}
+
+// fill the dynamic shared memory with quiet NaNs (checked builds)
+__device__ __forceinline__ void nsw_poison_smem(unsigned char* base) {
+  if constexpr (NSW_CHECKS) {
+    unsigned dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    for (unsigned q = threadIdx.x; q < dyn / 4; q += blockDim.x) reinterpret_cast<unsigned*>(base)[q] = 0x7fffffffu;
+    __syncthreads();
+  }
+}
 
 template <typename S>
 struct Fp;
@@ -232,6 +279,7 @@ __device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fi
 template <typename S, int M>
 __device__ __forceinline__ void lds_vec(S (&dst)[M], const S* src) {
   constexpr int V = Fp<S>::kVec;
+  nsw_check_smem(src, unsigned((M + V - 1) / V * 16));
   if constexpr (V == 4) {
 #pragma unroll
     for (int q = 0; q < (M + 3) / 4; ++q) {
@@ -256,6 +304,7 @@ __device__ __forceinline__ void lds_vec(S (&dst)[M], const S* src) {
 // vector once per row).
 template <typename S, int M>
 __device__ __forceinline__ void lds_vec_nc(S (&dst)[M], const S* src) {
+  nsw_check_smem(src, unsigned((M * sizeof(S) + 15) / 16 * 16));
   const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(src));
   if constexpr (sizeof(S) == 4) {
 #pragma unroll
@@ -284,6 +333,7 @@ template <typename S, int M>
 __device__ __forceinline__ void sts_vec(S* dst, const S (&src)[M]) {
   constexpr int V = Fp<S>::kVec;
   constexpr int P = Pitch<S, M>::value;
+  nsw_check_smem(dst, unsigned(P * sizeof(S)));
   if constexpr (V == 4) {
 #pragma unroll
     for (int q = 0; q < P / 4; ++q) {

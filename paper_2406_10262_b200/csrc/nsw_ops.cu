@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(OP_NT) fwd_chunk_op(const S* __restrict__ log_
                                                      double* __restrict__ res) {
   constexpr int P = Pitch<S, M>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  nsw_poison_smem(smem_raw);
   S* vv = reinterpret_cast<S*>(smem_raw);   // [P]   (16-byte aligned vectors first)
   S* red = vv + P;                          // [NW][P]
   S* Kt = red + OP_NW * P;                  // [n][P]
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(OP_NT) finish_op(const S* __restrict__ log_ker
                                                   double* __restrict__ resid) {
   constexpr int P = Pitch<S, M>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  nsw_poison_smem(smem_raw);
   S* vp = reinterpret_cast<S*>(smem_raw);   // [P] v~^{ts-1}
   S* vs = vp + P;                           // [P] v~^{ts}
   S* red = vs + P;                          // [NW][P]
@@ -238,6 +240,7 @@ __global__ void __launch_bounds__(OP_NT) sinkhorn_bwd_op(const S* __restrict__ l
                                                        int B, int n, int m, int T, S* __restrict__ grad_kernel) {
   constexpr int P = Pitch<S, M>::value;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  nsw_poison_smem(smem_raw);
   S* cvs = reinterpret_cast<S*>(smem_raw);  // [P]   (16-byte aligned vectors first)
   S* red = cvs + P;                         // [NW][P]
   S* Kt = red + OP_NW * P;                  // [n][P]
@@ -258,6 +261,10 @@ __global__ void __launch_bounds__(OP_NT) sinkhorn_bwd_op(const S* __restrict__ l
     if (k < m) v = t == 0 ? S(1) : Fp<S>::exp_(hist_all[(size_t(t - 1) * B + b) * m + k] - lvi[k]);
     vh[idx] = v;
   }
+  // padding columns of the column-VJP vector stay 0 (the row dots read all M
+  // slots; 0 * uninitialised shared memory could be NaN -- found by the
+  // checked build's NaN-poisoned shared memory)
+  if (threadIdx.x < P) cvs[threadIdx.x] = S(0);
   __syncthreads();
   // seed W = grad_plan * plan (sinkhorn.py:272-275); u~^T from log_u_final
   S c[M];

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   namespace cg = cooperative_groups;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  nsw_poison_smem(smem_raw);
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NR][CG][SP] lane segments + [NR][CG][TL] tails
   S* vr = Kt + size_t(Tl::KT);             // [4][P] ring of v~ history rows (row t in slot t & 3)

@@ -160,7 +160,11 @@ __device__ __forceinline__ void umma_commit(uint32_t mbar) {
 }
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
   uint32_t done = 0;
+  [[maybe_unused]] unsigned polls = 0;
   while (!done) {
+    if constexpr (NSW_CHECKS) {
+      if (++polls > (1u << 28)) nsw_check_fail("mbarrier wait timed out", mbar, parity);
+    }
     asm volatile(
         "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}\n"
         : "=r"(done)
@@ -231,6 +235,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   constexpr bool RANK1 = sizeof(S) == 4;
   static_assert(NT % 32 == 0 && M <= NT && P <= NT, "tile shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  nsw_poison_smem(smem_raw);
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K / K~ / gK rows
   S* vh = Kt + size_t(NT) * R * P;          // [T+1][P]   v~ history
