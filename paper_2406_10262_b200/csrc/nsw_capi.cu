@@ -1151,7 +1151,14 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
              s->T);
     return fail(NSW_ERR_SOLVER, msg);
   }
-  if (err & ERR_IMPACT) return fail(NSW_ERR_DOMAIN, "item impact became nonpositive during the solve");
+  if (err & ERR_IMPACT) {
+    if (s->dtype == NSW_F32)
+      return fail(NSW_ERR_DOMAIN,
+                  "item impact became nonpositive during the solve: the float32 Sinkhorn scalings left the fp32 "
+                  "exponent range (small epsilon" + std::string(s->cfg.warm_start ? "" : " with warm_start=False") +
+                      "); use DeviceOptions(dtype='float64') or warm_start=True");
+    return fail(NSW_ERR_DOMAIN, "item impact became nonpositive during the solve");
+  }
   return NSW_OK;
 }
 

@@ -236,3 +236,44 @@ def test_fp32_small_shapes_close_to_oracle(U, n, m, T, outer, eps):
     # there -- the policy itself still matches
     if U > 1:
         assert df <= 2e-6, df
+
+
+def test_cfg1_long_fp64_vs_reference(golden):
+    """the config-1 generator's first 100 users, 200 outer steps x
+    100 inner iterations (eps 0.05), against the reference's own run
+    (tests/golden/cfg1_long.npz, oracle/gen_golden.py cfg1long; its
+    item-permuted twin puts the reference's reorder noise floor at
+    8.5e-10 on X and 4e-14 on F)."""
+    g = golden("cfg1_long")
+    x, tr = _solve(g["relevance"], g["exposure"], float(g["epsilon"]), int(g["inner"]), int(g["outer"]), F64)
+    assert len(tr) == int(g["outer"])
+    dx = np.abs(x[:8] - g["policy_head"]).max()
+    w = np.linspace(0.5, 1.5, x.shape[1] * x.shape[2]).reshape(x.shape[1], x.shape[2])
+    U = x.shape[0]
+    cs = np.stack([x.reshape(U, -1).sum(1), (x * x).reshape(U, -1).sum(1), (x * w[None]).reshape(U, -1).sum(1)], 1)
+    dcs = np.abs(cs - g["policy_checksums"]).max()
+    df = np.abs(np.array(tr.objective) / g["objective"] - 1).max()
+    dg = np.abs(np.array(tr.grad_norm) / g["grad_norm"] - 1).max()
+    print(f"cfg1 100x200 fp64: max|dX|(8 users)={dx:.2e} checksums {dcs:.2e} rel dF={df:.2e} rel dgnorm={dg:.2e} "
+          f"(reference floor X {float(g['noise_floor']):.1e}, F {float(g['noise_floor_objective']):.1e})")
+    assert dx <= 1e-5 and dcs <= 1e-5
+    assert df <= 1e-6 and dg <= 1e-6
+    assert np.array_equal(orc.top_positions(x), g["top_positions"])
+
+
+def test_cfg1_full_fp32_trace_vs_fp64_device():
+    """Full-size config 1 (1000 x 500 x 11, eps 0.05, 100 inner) for 50 outer
+    steps: the fp32 throughput instantiation's objective trace against the
+    float64 instantiation on the same inputs (relative 1e-5), and a finite,
+    feasible policy."""
+    from paper_2406_10262_b200.data import make_instance
+    rel, expo, cfg = make_instance("cfg1")
+    x32, t32 = _solve(rel, expo, cfg.epsilon, cfg.inner_iters, 50, F32)
+    x64, t64 = _solve(rel, expo, cfg.epsilon, cfg.inner_iters, 50, F64)
+    df = np.abs(np.array(t32.objective) / np.array(t64.objective) - 1)
+    print(f"cfg1 full fp32 vs fp64 device, 50 steps: max rel dF={df.max():.2e} (step {int(df.argmax())}), "
+          f"final |dX|={np.abs(x32 - x64).max():.2e}")
+    assert df.max() <= 1e-5
+    assert np.isfinite(x32).all()
+    col = x32.sum(axis=1)
+    assert np.abs(col[:, :-1] - 1).max() < 2e-4
