@@ -5,6 +5,9 @@
 #include "nsw_registry.h"
 #include "nsw_step_kernel.cuh"
 
+#ifndef NSW_EXP_TILES
+#define NSW_EXP_TILES 0
+#endif
 #ifndef NSW_M
 #error "NSW_M must be defined"
 #endif
@@ -75,6 +78,11 @@ NSW_REG(8, 128, 3)
 NSW_REG(8, 256, 1)   // (4, 512, 1): 16 warps, 11 % slower on config 3 (profiles/r01d_row_tiles_cfg2_cfg3.txt)
 NSW_REG(2, 256, 1)
 NSW_REG(1, 512, 1)
+#if NSW_EXP_TILES   // A/B builds only: 9-13-warp row tiles for config 3
+NSW_REG(6, 352, 1)
+NSW_REG(7, 288, 1)
+NSW_REG(5, 416, 1)
+#endif
 #elif NSW_M <= 16
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
@@ -93,6 +101,11 @@ NSW_REG(4, 128, 1)
 NSW_REG(4, 256, 1)
 NSW_REG(2, 256, 1)
 NSW_REG(2, 512, 1)
+#if NSW_EXP_TILES   // A/B builds only: 7-12-warp row tiles for config 2
+NSW_REG(3, 384, 1)
+NSW_REG(4, 288, 1)
+NSW_REG(5, 224, 1)
+#endif
 #else
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
