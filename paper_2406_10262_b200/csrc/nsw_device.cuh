@@ -275,6 +275,43 @@ __device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fi
   __syncthreads();
 }
 
+// Same reduction with the finished vector delivered to EVERY thread in
+// registers (M <= 32): after the warp reduce-scatter and one barrier, every
+// warp sums the per-warp partials in warp order itself (lane k: column k) and
+// applies fval(k, total), and the values are spread over the warp by shuffles.
+// One barrier instead of two and no shared-memory round trip of the result;
+// the same summation order, so bitwise identical to cta_reduce_cols.  `red`
+// must be double-buffered by the caller across consecutive calls ([2][NW][M]:
+// a warp may store the next call's partials while a slower one still reads).
+#ifndef NSW_BCAST
+#define NSW_BCAST 0   // measured slower on configs 1-3 (profiles/r02/ab_bcast_reduce.txt)
+#endif
+template <typename S, int M, int NT, class FVal>
+__device__ __forceinline__ void cta_reduce_cols_bcast(S (&v)[M], S* red, int m, FVal fval, S (&out)[M]) {
+  static_assert(M <= 32, "one column per lane");
+  constexpr int NW = NT / 32;
+  int lane;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+  const int warp = threadIdx.x >> 5;
+  int base = 0, lim = M;
+  reduce_scatter<S, M, M, 16, OpSum>(v, lane, base, lim);
+  if (base < lim && base < m) red[warp * M + base] = v[0];
+  if constexpr (NW == 1) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+  S val = S(0);
+  if (lane < m) {
+    S acc = red[lane];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) acc = acc + red[w * M + lane];
+    val = fval(lane, acc);
+  }
+#pragma unroll
+  for (int k = 0; k < M; ++k) out[k] = __shfl_sync(0xffffffffu, val, k);
+}
+
 // Load an M-vector from shared memory (16-byte vector loads; pitch padded).
 template <typename S, int M>
 __device__ __forceinline__ void lds_vec(S (&dst)[M], const S* src) {

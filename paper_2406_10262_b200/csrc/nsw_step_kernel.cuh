@@ -121,7 +121,7 @@ template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = RowPitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
-  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + size_t(NT / 32) * P + 3 * P + rows + 2 * P +
+  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + 2 * size_t(NT / 32) * P + 3 * P + rows + 2 * P +
                       size_t(NT / 32) + 4 + (stage_inputs<S, NT, MINB>() ? 2 * size_t(NT) * R : 0) + P) +
          32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
          16 +                   // mbarrier of the cost tile's bulk copy
@@ -239,8 +239,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K / K~ / gK rows
   S* vh = Kt + size_t(NT) * R * P;          // [T+1][P]   v~ history
-  S* red = vh + size_t(T + 1) * P;          // [NW][P]    column partials
-  S* vec0 = red + NW * P;                   // [P] scaling vector / cv
+  S* red = vh + size_t(T + 1) * P;          // [2][NW][P] column partials (double-buffered)
+  S* vec0 = red + 2 * NW * P;               // [P] scaling vector / cv
   S* vec1 = vec0 + P;                       // [P] beta / column max
   S* vec2 = vec1 + P;                       // [P] warm-start duals lvi
   S* rowA = vec2 + P;                       // [NT*R] (no padding column only)
@@ -783,11 +783,20 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       // steady-state body is branch-free.  Padding rows (K~ row = 0) get a
       // finite u~ from the clamped reciprocal, hence h = 0 and no column
       // contribution; their G is discarded in the epilogue.
+      // cv of the current level: in registers of every thread, delivered by
+      // the previous level's broadcast reduction (NSW_BCAST) or from vec0
+      S cvr[M];
+      if constexpr (NSW_BCAST) lds_vec<S, M>(cvr, vec0);
       auto level = [&](const int t, auto first_c, auto last_c) {
         constexpr bool FIRST = decltype(first_c)::value;
         constexpr bool LAST = decltype(last_c)::value;
         S cv[M], vp[M], c[M];
-        lds_vec<S, M>(cv, vec0);
+        if constexpr (NSW_BCAST) {
+#pragma unroll
+          for (int k = 0; k < M; ++k) cv[k] = cvr[k];
+        } else {
+          lds_vec<S, M>(cv, vec0);
+        }
         const S* vpp1 = vh + size_t(t - 1) * P;
         if constexpr (!LEAN) lds_vec<S, M>(vp, vpp1);
         const S* vppp = vh + size_t(LAST ? 0 : t - 2) * P;
@@ -814,11 +823,22 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
         if constexpr (!LAST) {
-          cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-            const S vpk = vh[size_t(t - 1) * P + k];
-            const S gv = -mul_(vpk, tot);
-            vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
-          });
+          if constexpr (NSW_BCAST) {
+            cta_reduce_cols_bcast<S, M, NT>(
+                c, red + (t & 1) * NW * M, m,
+                [&](int k, S tot) -> S {
+                  const S vpk = vh[size_t(t - 1) * P + k];
+                  const S gv = -mul_(vpk, tot);
+                  return mul_(mul_(vpk, gv), inv_mass(k));
+                },
+                cvr);
+          } else {
+            cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
+              const S vpk = vh[size_t(t - 1) * P + k];
+              const S gv = -mul_(vpk, tot);
+              vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
+            });
+          }
         }
       };
       if (Th == 1) {
@@ -1030,6 +1050,33 @@ forward_iterations:
     // no residual bookkeeping at all
     auto iterate = [&](auto tol_c) {
       constexpr bool TOLM = decltype(tol_c)::value;
+      if constexpr (!TOLM && NSW_BCAST) {
+        // fixed schedule: v~ stays in registers; one barrier per iteration
+        S vv[M];
+        lds_vec<S, M>(vv, vec0);
+        for (int t = t_start; t <= t_end; ++t) {
+          S c[M];
+#pragma unroll
+          for (int r = 0; r < R; ++r) ut[r] = rcp_clamped(rdot<S, M, CH, PK>(A[r], vv));
+#pragma unroll
+          for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+          for (int r = 0; r < R; ++r) axpy_<S, M, PK>(c, A[r], ut[r]);
+          cta_reduce_cols_bcast<S, M, NT>(
+              c, red + (t & 1) * NW * M, m,
+              [&](int k, S tot) -> S {
+                const S vn = F::div_fast(mass(k), tot);
+                if (warp == 0) {
+                  vec0[k] = vn;
+                  hu[size_t(t) * m + k] = vn;
+                }
+                return vn;
+              },
+              vv);
+        }
+        __syncthreads();   // warp 0's last vec0 before the impact terms read it
+        return;
+      }
       for (int t = t_start; t <= t_end; ++t) {
         S vv[M], c[M];
         lds_vec<S, M>(vv, vec0);
