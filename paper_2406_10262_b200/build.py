@@ -31,7 +31,7 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
 INSTANCES = [(f64, M) for f64 in (0, 1) for M in (4, 8, 11, 16, 21, 32)]
 
 HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_registry.h", "nsw_step_generic.cuh",
-           "nsw_generic.h"]
+           "nsw_generic.h", "nsw_pool.h"]
 
 
 def _nvcc():

@@ -19,6 +19,7 @@
 
 #include "../../include/nswrank_b200.h"
 #include "nsw_generic.h"
+#include "nsw_pool.h"
 #include "nsw_registry.h"
 #include "nsw_step_kernel.cuh"
 
@@ -391,30 +392,9 @@ nsw_status read_state(nsw_solver* s) {
   return NSW_OK;
 }
 
-// Device memory of the solvers comes from a private stream-ordered pool per
-// device (created once, keeps its memory between solvers so a repeated solve
-// of the same size allocates without OS calls); the device's default pool,
-// which torch or other cudaMallocAsync users may share, is left untouched.
-// nsw_release_cached() trims it.
-std::mutex g_pool_mu;
-cudaMemPool_t g_pool[64] = {};
-
-cudaMemPool_t solver_pool(int device) {
-  if (device < 0 || device >= 64) return nullptr;
-  std::lock_guard<std::mutex> lk(g_pool_mu);
-  if (!g_pool[device]) {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = device;
-    cudaMemPool_t p = nullptr;
-    if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
-    uint64_t keep = ~uint64_t(0);
-    cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep);
-    g_pool[device] = p;
-  }
-  return g_pool[device];
-}
+// Device memory of the solvers comes from the library's private pool
+// (nsw_pool.h).
+cudaMemPool_t solver_pool(int device) { return private_pool(device); }
 
 #if NSW_CHECKS
 // checked builds: 64 KB canary bands on both sides of every solver buffer,
@@ -586,12 +566,13 @@ void nsw_release_cached(void) {
     g_host_free.clear();
     g_host_cached = 0;
   }
-  std::lock_guard<std::mutex> lk(g_pool_mu);
+  PoolTable& t = pool_table();
+  std::lock_guard<std::mutex> lk(t.mu);
   for (int d = 0; d < 64; ++d)
-    if (g_pool[d]) {
+    if (t.pool[d]) {
       DeviceGuard guard(d);
       cudaDeviceSynchronize();
-      cudaMemPoolTrimTo(g_pool[d], 0);
+      cudaMemPoolTrimTo(t.pool[d], 0);
     }
 }
 
@@ -1441,7 +1422,7 @@ nsw_status nsw_solver_metrics(nsw_solver* s, double threshold, double* out_host)
           : nsw_policy_metrics_f32((const float*)s->xbest, (const float*)s->rel, s->expo_host.data(), s->U, s->n,
                                    s->m, threshold, out_host, s->stream);
   if (e != NSW_OK) return fail(e, "policy metrics failed");
-  s->launches += 5;
+  s->launches += 6;   // masses, impact partials + combine, envy GEMM + combine, finish
   return NSW_OK;
 }
 

@@ -5,11 +5,11 @@
 //   items_better_off = mean_i [ Imp_i > (1 + th) Imp^unif_i ]
 //   items_worse_off  = mean_i [ Imp_i < (1 - th) Imp^unif_i ]
 // Everything is accumulated in float64 in a fixed order (deterministic).
-// The one dense product (cross, n x n x |U|) is a plain cuBLAS DGEMM; the
-// allocation masses, impacts and row maxima are kernels here.
-#include <cublas_v2.h>
+// The one dense product (cross = R' A, n x n x |U|, reference metrics.py:38)
+// never materialises: envy_gemm_kernel runs it on the FP64 tensor cores
+// (mma.sync m8n8k4 f64, DMMA) with the row maximum and the diagonal fused
+// into the epilogue, so only [n / 64][n] partial maxima reach HBM.
 #include <cuda_runtime.h>
-#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -17,14 +17,10 @@
 
 #include "../../include/nswrank_b200.h"
 #include "nsw_device.cuh"
+#include "nsw_pool.h"
 
 namespace nsw {
 namespace {
-
-__global__ void widen_to_f64(const float* __restrict__ src, double* __restrict__ dst, size_t n) {
-  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    dst[i] = double(src[i]);
-}
 
 // A_uj = sum_{k<m-1} x_ujk e_k  (float64), one thread per (u, j)
 template <typename S>
@@ -73,13 +69,154 @@ __global__ void impact_combine_kernel(const double* __restrict__ pa, const doubl
   imp_unif[j] = b * e_sum_over_n;
 }
 
-// envy_i = max_j cross(i, j) - cross(i, i); cross column-major (n x n)
-__global__ void envy_kernel(const double* __restrict__ cross, int n, double* __restrict__ envy) {
+// ---------------------------------------------------------------------------
+// envy_i = max_j cross(i, j) - cross(i, i),  cross(i, j) = sum_u r_ui A_uj
+// (reference metrics.py:38-41), as one fused FP64 tensor-core GEMM.
+// CTA: 64 x 64 output tile (4 warps, 2 x 2 warp tiles of 32 x 32 = 4 x 4 DMMA
+// m8n8k4 tiles), users staged 16 at a time through shared memory (both
+// operands are [U][n] row-major: coalesced 64-item rows), the next stage
+// prefetched into registers during the MMAs.  Epilogue: row maxima over the
+// tile's 64 columns -> part[jt][i]; diagonal tiles also write cross(i, i).
+// The user sum runs in index order (fixed): deterministic.
+// ---------------------------------------------------------------------------
+constexpr int EG_T = 64;       // output tile edge
+constexpr int EG_KS = 16;      // users per shared-memory stage
+constexpr int EG_P = 72;       // padded row pitch (doubles): conflict-free fragment loads
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Split-K (few output tiles, e.g. n = 500): blockIdx.z takes users
+// [z U / S, (z + 1) U / S) and writes its partial 64 x 64 tile to
+// pcross[z][i][j] (pcross != nullptr); envy_splitk_combine sums the splits in
+// split order, then takes the row maxima and the diagonal.
+template <typename S>
+__global__ void __launch_bounds__(128) envy_gemm_kernel(const S* __restrict__ rel, const double* __restrict__ A,
+                                                        int U, int n, double* __restrict__ part,
+                                                        double* __restrict__ diag, double* __restrict__ pcross) {
+  __shared__ __align__(16) double sR[EG_KS][EG_P];   // r_ui  (k = user, i = row item)
+  __shared__ __align__(16) double sA[EG_KS][EG_P];   // A_uj  (k = user, j = column item)
+  __shared__ double smax[2][EG_T];
+  const int it = blockIdx.y, jt = blockIdx.x;
+  const int i0 = it * EG_T, j0 = jt * EG_T;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wi = warp >> 1, wj = warp & 1;   // warp tile (rows wi*32.., columns wj*32..)
+  const int g = lane >> 2, q = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  // each thread stages 8 elements of each operand per stage: rows k = tid/16 + 8e, 4 items at (tid%16)*4
+  const int lk = tid >> 4, li = (tid & 15) * 4;
+  double pr[2][4], pa[2][4];
+  auto fetch = [&](int u0) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int u = u0 + lk + 8 * e;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int i = i0 + li + c, j = j0 + li + c;
+        pr[e][c] = (u < U && i < n) ? double(rel[size_t(u) * n + i]) : 0.0;
+        pa[e][c] = (u < U && j < n) ? A[size_t(u) * n + j] : 0.0;
+      }
+    }
+  };
+  const int ub = int((long long)U * blockIdx.z / gridDim.z), ue = int((long long)U * (blockIdx.z + 1) / gridDim.z);
+  U = ue;   // fetch() masks users >= U
+  fetch(ub);
+  for (int u0 = ub; u0 < ue; u0 += EG_KS) {
+    __syncthreads();   // the previous stage's fragments are consumed
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        sR[lk + 8 * e][li + c] = pr[e][c];
+        sA[lk + 8 * e][li + c] = pa[e][c];
+      }
+    __syncthreads();
+    if (u0 + EG_KS < U) fetch(u0 + EG_KS);   // next stage in flight during the MMAs
+#pragma unroll
+    for (int k0 = 0; k0 < EG_KS; k0 += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        af[t] = sR[k0 + q][wi * 32 + t * 8 + g];   // A fragment: row g, column (user) q
+        bf[t] = sA[k0 + q][wj * 32 + t * 8 + g];   // B fragment: row (user) q, column g
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma_m8n8k4(acc[a][b], af[a], bf[b]);
+    }
+  }
+  // epilogue: accumulator (a, b, c) is cross(i0 + wi*32 + a*8 + g, j0 + wj*32 + b*8 + 2q + c)
+  if (pcross != nullptr) {
+    double* pc = pcross + size_t(blockIdx.z) * n * n;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int i = i0 + wi * 32 + a * 8 + g, j = j0 + wj * 32 + b * 8 + 2 * q + c;
+          if (i < n && j < n) pc[size_t(i) * n + j] = acc[a][b][c];
+        }
+    return;
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int il = wi * 32 + a * 8 + g;
+    double mx = -INFINITY;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int jl = wj * 32 + b * 8 + 2 * q + c;
+        if (j0 + jl < n) mx = fmax(mx, acc[a][b][c]);
+        if (it == jt && il == jl && i0 + il < n) diag[i0 + il] = acc[a][b][c];
+      }
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    if (q == 0) smax[wj][il] = mx;
+  }
+  __syncthreads();
+  if (tid < EG_T && i0 + tid < n) part[size_t(jt) * n + i0 + tid] = fmax(smax[0][tid], smax[1][tid]);
+}
+
+__global__ void envy_splitk_combine(const double* __restrict__ pcross, int n, int splits,
+                                    double* __restrict__ envy) {
+  const int i = blockIdx.x;
+  __shared__ double smx[128];
+  double mx = -INFINITY;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double c = 0.0;
+    for (int z = 0; z < splits; ++z) c += pcross[(size_t(z) * n + i) * n + j];
+    mx = fmax(mx, c);
+  }
+  smx[threadIdx.x] = mx;
+  __syncthreads();
+  for (int w = 64; w > 0; w >>= 1) {
+    if (threadIdx.x < w) smx[threadIdx.x] = fmax(smx[threadIdx.x], smx[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double d = 0.0;
+    for (int z = 0; z < splits; ++z) d += pcross[(size_t(z) * n + i) * n + i];
+    envy[i] = smx[0] - d;
+  }
+}
+
+__global__ void envy_combine_kernel(const double* __restrict__ part, const double* __restrict__ diag, int n,
+                                    int tiles, double* __restrict__ envy) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double mx = -INFINITY;
-  for (int j = 0; j < n; ++j) mx = fmax(mx, cross[size_t(j) * n + i]);
-  envy[i] = mx - cross[size_t(i) * n + i];
+  for (int t = 0; t < tiles; ++t) mx = fmax(mx, part[size_t(t) * n + i]);
+  envy[i] = mx - diag[i];
 }
 
 // one block: the four metrics from the per-item vectors, fixed-order sums
@@ -118,43 +255,6 @@ __global__ void metrics_finish_kernel(const double* __restrict__ imp, const doub
   }
 }
 
-// cuBLAS is loaded on first use (dlopen), so the solver library does not pull
-// it in at import time; only the envy product of the metrics needs it.
-struct Cublas {
-  using create_t = cublasStatus_t (*)(cublasHandle_t*);
-  using stream_t = cublasStatus_t (*)(cublasHandle_t, cudaStream_t);
-  using dgemm_t = cublasStatus_t (*)(cublasHandle_t, cublasOperation_t, cublasOperation_t, int, int, int,
-                                     const double*, const double*, int, const double*, int, const double*, double*,
-                                     int);
-  create_t create = nullptr;
-  stream_t set_stream = nullptr;
-  dgemm_t dgemm = nullptr;
-  bool ok = false;
-  Cublas() {
-    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_LOCAL);
-    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_LOCAL);
-    if (!h) return;
-    create = reinterpret_cast<create_t>(dlsym(h, "cublasCreate_v2"));
-    set_stream = reinterpret_cast<stream_t>(dlsym(h, "cublasSetStream_v2"));
-    dgemm = reinterpret_cast<dgemm_t>(dlsym(h, "cublasDgemm_v2"));
-    ok = create && set_stream && dgemm;
-  }
-};
-
-const Cublas& cublas() {
-  static const Cublas c;
-  return c;
-}
-
-// one cuBLAS handle per host thread and device (creating one costs ms)
-cublasHandle_t cublas_handle() {
-  thread_local cublasHandle_t handles[64] = {};
-  int dev = 0;
-  if (!cublas().ok || cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-  if (!handles[dev] && cublas().create(&handles[dev]) != CUBLAS_STATUS_SUCCESS) handles[dev] = nullptr;
-  return handles[dev];
-}
-
 template <typename S>
 nsw_status policy_metrics(const void* X, const void* rel, const double* expo_host, int32_t U, int32_t n,
                           int32_t m, double threshold, double* out_host, void* stream) {
@@ -164,21 +264,16 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   const size_t cells = size_t(U) * n;
   // user chunks of the impact sums: ~4 CTAs of 128 items per SM
   const int chunks = std::max(1, std::min(U, (sm_count() * 4 * 128 + n - 1) / n));
-  double* buf = nullptr;   // e[m] | A[U n] | cross[n n] | imp[n] | unif[n] | envy[n] | out[4] | pa, pb [chunks n]
-  const size_t words = size_t(m) + cells + size_t(n) * n + 3 * size_t(n) + 4 + 2 * size_t(chunks) * n;
-  {
-    // keep the pool's memory between calls (large transient buffers)
-    int dev = 0;
-    cudaMemPool_t pool;
-    uint64_t keep = ~uint64_t(0);
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  }
-  if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  const int tiles = (n + EG_T - 1) / EG_T;
+  // e[m] | A[U n] | part[tiles n] | diag[n] | imp[n] | unif[n] | envy[n] | out[4] | pa, pb [chunks n]
+  double* buf = nullptr;
+  const size_t words = size_t(m) + cells + size_t(tiles) * n + 4 * size_t(n) + 4 + 2 * size_t(chunks) * n;
+  if (private_malloc((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
   double* e = buf;
   double* A = e + m;
-  double* cross = A + cells;
-  double* imp = cross + size_t(n) * n;
+  double* part = A + cells;
+  double* diag = part + size_t(tiles) * n;
+  double* imp = diag + n;
   double* unif = imp + n;
   double* envy = unif + n;
   double* out = envy + n;
@@ -187,8 +282,6 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
   double esum = 0.0;
   for (int k = 0; k < m - 1; ++k) esum += expo_host[k];
   nsw_status status = NSW_OK;
-  cublasHandle_t h = nullptr;
-  const double one = 1.0, zero = 0.0;
   if (cudaMemcpyAsync(e, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {
     status = NSW_ERR_CUDA;
   } else {
@@ -196,31 +289,23 @@ nsw_status policy_metrics(const void* X, const void* rel, const double* expo_hos
     impact_partial_kernel<S><<<dim3((n + 127) / 128, chunks), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n,
                                                                              chunks, pa, pb);
     impact_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(pa, pb, n, chunks, esum / n, imp, unif);
-    // cross(i, j) = sum_u r_ui A_uj: column-major n x n = R' A with R, A
-    // read as column-major n x U matrices (their row-major [U][n] layout)
-    double* Rd = nullptr;
-    if constexpr (sizeof(S) == 8) {
-      Rd = const_cast<double*>(static_cast<const double*>(rel));
-    } else {
-      // widen R for DGEMM (float64 products, as the reference's numpy matmul)
-      if (cudaMallocAsync((void**)&Rd, cells * sizeof(double), st) != cudaSuccess) status = NSW_ERR_CUDA;
-      else widen_to_f64<<<sm_count() * 8, 256, 0, st>>>(static_cast<const float*>(rel), Rd, cells);
-    }
-    if (status == NSW_OK && (h = cublas_handle()) == nullptr) status = NSW_ERR_CUDA;
-    if (status == NSW_OK && cublas().set_stream(h, st) != CUBLAS_STATUS_SUCCESS) status = NSW_ERR_CUDA;
-    if (status == NSW_OK && cublas().dgemm(h, CUBLAS_OP_N, CUBLAS_OP_T, n, n, U, &one, Rd, n, A, n, &zero, cross,
-                                           n) != CUBLAS_STATUS_SUCCESS)
+    // envy: the fused FP64 tensor-core product R' A with row maxima / diagonal
+    // few output tiles: split the user sum so about two CTAs per SM run
+    const int splits = std::max(1, std::min((2 * sm_count() + tiles * tiles - 1) / (tiles * tiles), (U + 63) / 64));
+    double* pcross = nullptr;
+    if (splits > 1 && private_malloc((void**)&pcross, size_t(splits) * n * n * sizeof(double), st) != cudaSuccess)
       status = NSW_ERR_CUDA;
     if (status == NSW_OK) {
-      envy_kernel<<<(n + 127) / 128, 128, 0, st>>>(cross, n, envy);
-      metrics_finish_kernel<<<1, 256, 0, st>>>(imp, unif, envy, n, U, threshold, out);
-      if (cudaGetLastError() != cudaSuccess ||
-          cudaMemcpyAsync(out_host, out, 4 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        status = NSW_ERR_CUDA;
+      envy_gemm_kernel<S><<<dim3(tiles, tiles, splits), 128, 0, st>>>(static_cast<const S*>(rel), A, U, n, part,
+                                                                        diag, pcross);
+      if (splits > 1) envy_splitk_combine<<<n, 128, 0, st>>>(pcross, n, splits, envy);
+      else envy_combine_kernel<<<(n + 127) / 128, 128, 0, st>>>(part, diag, n, tiles, envy);
     }
-    if constexpr (sizeof(S) == 4) {
-      if (Rd) cudaFreeAsync(Rd, st);
-    }
+    if (pcross) cudaFreeAsync(pcross, st);
+    metrics_finish_kernel<<<1, 256, 0, st>>>(imp, unif, envy, n, U, threshold, out);
+    if (cudaGetLastError() != cudaSuccess ||
+        cudaMemcpyAsync(out_host, out, 4 * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      status = NSW_ERR_CUDA;
   }
   cudaFreeAsync(buf, st);
   if (cudaStreamSynchronize(st) != cudaSuccess) status = NSW_ERR_CUDA;
@@ -238,7 +323,7 @@ nsw_status policy_impact(const void* X, const void* rel, const double* expo_host
   const int chunks = std::max(1, std::min(U, (sm_count() * 4 * 128 + n - 1) / n));
   double* buf = nullptr;   // e[m] | A[U n] | imp[n] | unif[n] | pa, pb [chunks n]
   const size_t words = size_t(m) + cells + 2 * size_t(n) + 2 * size_t(chunks) * n;
-  if (cudaMallocAsync((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  if (private_malloc((void**)&buf, words * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
   double* e = buf;
   double* A = e + m;
   double* imp = A + cells;
@@ -282,7 +367,7 @@ nsw_status welfare_gradient(const void* rel, const double* expo_host, const doub
   if (U <= 0 || n <= 0 || m < 2) return NSW_ERR_SHAPE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   double* buf = nullptr;
-  if (cudaMallocAsync((void**)&buf, (size_t(m) + n) * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
+  if (private_malloc((void**)&buf, (size_t(m) + n) * sizeof(double), st) != cudaSuccess) return NSW_ERR_CUDA;
   nsw_status status = NSW_OK;
   if (cudaMemcpyAsync(buf, expo_host, size_t(m - 1) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess ||
       cudaMemcpyAsync(buf + m, imp_host, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, st) != cudaSuccess) {

@@ -21,6 +21,7 @@
 
 #include "../../include/nswrank_b200.h"
 #include "nsw_device.cuh"
+#include "nsw_pool.h"
 
 namespace nsw {
 namespace {
@@ -371,9 +372,9 @@ nsw_status run_solve(const S* K, const S* row, const S* col, const S* lvi, int B
   double* res = nullptr;
   double* rd = nullptr;
   nsw_status e = NSW_OK;
-  if (cudaMallocAsync((void**)&vt, size_t(B) * (T + 1) * m * sizeof(S), st) != cudaSuccess ||
-      cudaMallocAsync((void**)&rd, size_t(B) * sizeof(double), st) != cudaSuccess ||
-      (tolm && cudaMallocAsync((void**)&res, size_t(B) * (T + 1) * sizeof(double), st) != cudaSuccess))
+  if (private_malloc((void**)&vt, size_t(B) * (T + 1) * m * sizeof(S), st) != cudaSuccess ||
+      private_malloc((void**)&rd, size_t(B) * sizeof(double), st) != cudaSuccess ||
+      (tolm && private_malloc((void**)&res, size_t(B) * (T + 1) * sizeof(double), st) != cudaSuccess))
     e = NSW_ERR_CUDA;
   int ts = T;
   if (e == NSW_OK) {
@@ -481,7 +482,7 @@ nsw_status cost_from_policy(const S* x, size_t count, double eps, S* out, void* 
   cudaStream_t st = (cudaStream_t)stream;
   unsigned* bad = nullptr;
   unsigned hbad = 0;
-  if (cudaMallocAsync((void**)&bad, sizeof(unsigned), st) != cudaSuccess) return NSW_ERR_CUDA;
+  if (private_malloc((void**)&bad, sizeof(unsigned), st) != cudaSuccess) return NSW_ERR_CUDA;
   cudaMemsetAsync(bad, 0, sizeof(unsigned), st);
   cost_from_policy_op<S><<<sm_count() * 4, 256, 0, st>>>(x, count, S(-eps), out, bad);
   cudaMemcpyAsync(&hbad, bad, sizeof(unsigned), cudaMemcpyDeviceToHost, st);

@@ -10,7 +10,9 @@ Same names and signatures as the reference (metrics.py:16-63):
 plus ``policy_metrics`` that returns all four from one device pass.  The
 allocation masses, impacts and row maxima are kernels in
 ``csrc/nsw_metrics.cu``; the one dense product of ``mean_max_envy``
-(n x n x |U|) is a cuBLAS DGEMM.  float64 accumulation throughout; a
+(n x n x |U|, metrics.py:38) is a hand-written FP64 tensor-core kernel
+(mma.sync m8n8k4 f64) with the row maxima fused into its epilogue, so the
+n x n matrix is never written.  float64 accumulation throughout; a
 float32 policy tensor (e.g. a device solve's output) is read as is.
 Inputs may be the reference-style objects, numpy arrays, or CUDA torch
 tensors already on the device.
