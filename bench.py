@@ -308,7 +308,17 @@ def run_ours(a):
     from paper_2406_10262_b200.solver import DeviceSolver, solve_fair_ranking
 
     cfg = BASELINE_CONFIGS[a.config]
-    if a.slice:
+    datagen = a.datagen or ("device" if a.config in ("cfg3", "cfg4") else "host")
+    if datagen == "device":
+        # on-device counter-based generator (csrc/nsw_datagen.cu): configs 3 / 4
+        # are slow or infeasible to draw on the host; the solver API takes host
+        # arrays, so the generated block is copied back once, outside timing
+        from paper_2406_10262_b200.datagen import make_instance_device
+        lo, hi = (int(x) for x in a.slice.split(":")) if a.slice else (0, a.users or cfg.num_users)
+        relt, expo, _ = make_instance_device(a.config, seed=0, user_slice=(lo, hi))
+        rel = relt.double().cpu().numpy()
+        del relt
+    elif a.slice:
         lo, hi = (int(x) for x in a.slice.split(":"))
         rel, expo, _ = make_instance(a.config, seed=0, user_slice=(lo, hi))
     else:
@@ -375,7 +385,7 @@ def run_ours(a):
     line = {"metric": "outer_ascent_iters_per_s", "value": value, "unit": "outer_iters/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_total / a.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if a.dtype == "float32" else "f64",
-            "data": "synthetic (BASELINE generator, seed 0)",
+            "data": f"synthetic (BASELINE generator, seed 0, {datagen})",
             "config": {"workload": _workload(a.config, U, n, m, cfg.epsilon, T), "schedule": "fixed (BASELINE)",
                        "users_per_gpu": users_local, "l2": "flushed between timed steps (1 GiB write, then discard of those lines)",
                        "tile": variant},
@@ -484,6 +494,9 @@ def main(argv=None):
     ap.add_argument("--inner", type=int, default=None)
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--slice", default=None, help="START:STOP users of the full instance (e.g. one GPU's shard)")
+    ap.add_argument("--datagen", default=None, choices=["host", "device"],
+                    help="input generator: numpy (host) or the on-device Philox generator (default: device for "
+                         "cfg3 / cfg4, host otherwise)")
     a = ap.parse_args(argv)
     if a.dtype is None:
         a.dtype = BASELINE_CONFIGS[a.config].dtype

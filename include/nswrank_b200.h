@@ -291,6 +291,21 @@ void nsw_host_free(void* ptr);
  * part of the solvers' private device pools (trimmed to zero). */
 void nsw_release_cached(void);
 
+/* On-device generation of the BASELINE synthetic relevance (counter-based
+ * Philox4x32-10: every value a pure function of (seed, stream, index), so a
+ * rank generates exactly its user shard [user0, user0 + users)); out is a
+ * device [users][n] array of `dtype` (fp32 values are rounded once, clamped
+ * to [1e-6, 1]).  Replaces the host generators for configs 1-4
+ * (the reference's own generator is data.py:30-52).
+ *   latent: r = sigmoid(<p_u, q_i> + b_i), p, q ~ N(0, I/d); bias_kind 0 none,
+ *           1 N(0, bias_scale), 2 LogNormal(0, bias_scale) mean-centred.
+ *   sparse: per_user distinct items ~ rank^-zipf_s (Gumbel-top-k), r ~ Beta(2, 5),
+ *           every other entry floor_value. */
+nsw_status nsw_datagen_latent(int64_t user0, int32_t users, int32_t n, int32_t d, int32_t bias_kind,
+                              double bias_scale, uint64_t seed, int32_t dtype, void* out, void* stream);
+nsw_status nsw_datagen_sparse(int64_t user0, int32_t users, int32_t n, int32_t per_user, double zipf_s,
+                              double floor_value, uint64_t seed, int32_t dtype, void* out, void* stream);
+
 /* Whether a (dtype, n, m, iters) problem runs on the device: every shape the
  * reference accepts (2 <= m <= n, reference core.py:60-66) does. */
 int32_t nsw_supported(int32_t dtype, int32_t num_items, int32_t num_positions, int32_t iters);

@@ -15,6 +15,7 @@ _EXPORTS = {
     "solver": ("SolveTrace", "DeviceOptions", "DeviceSolver", "solve_fair_ranking", "NativeLibraryError",
                "impact", "nsw_objective", "nsw_gradient_wrt_policy", "AdamState", "adam_update"),
     "data": ("exposure_model", "make_instance", "BASELINE_CONFIGS"),
+    "datagen": ("generate_relevance", "make_instance_device"),
     "sinkhorn": ("sinkhorn_batch", "sinkhorn_backward_batch", "sinkhorn_batch_solve", "Marginals", "SinkhornState",
                  "sinkhorn_solve", "sinkhorn_backward", "cost_from_policy"),
     "ranking": ("top_positions",),

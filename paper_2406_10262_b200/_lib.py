@@ -50,6 +50,9 @@ SIGNATURES = {
     "nsw_version": (C.c_char_p, []),
     "nsw_supported": (_i32, [_i32, _i32, _i32, _i32]),
     "nsw_tiled": (_i32, [_i32, _i32, _i32, _i32]),
+    "nsw_datagen_latent": (C.c_int, [C.c_int64, _i32, _i32, _i32, _i32, C.c_double, C.c_uint64, _i32, _vp, _vp]),
+    "nsw_datagen_sparse": (C.c_int, [C.c_int64, _i32, _i32, _i32, C.c_double, C.c_double, C.c_uint64, _i32, _vp,
+                                     _vp]),
     "nsw_solve_fair_ranking": (C.c_int, [_dp, _dp, _i32, _i32, _i32, C.POINTER(SolverConfigC),
                                          C.POINTER(DeviceOptionsC), _dp, C.POINTER(TraceC)]),
     "nsw_solver_create": (C.c_int, [_dp, _dp, _i32, _i32, _i32, _dp, _i32, C.POINTER(SolverConfigC),

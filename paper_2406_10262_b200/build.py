@@ -55,7 +55,7 @@ def _jobs(build_dir=BUILD):
     for f64 in (0, 1):
         jobs.append((os.path.join(CSRC, "nsw_inst_cl.cu"), os.path.join(build_dir, f"inst_cl_{'f64' if f64 else 'f32'}.o"),
                      [f"-DNSW_F64={f64}"]))
-    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics", "nsw_generic"):
+    for name in ("nsw_common", "nsw_capi", "nsw_ops", "nsw_rank", "nsw_metrics", "nsw_generic", "nsw_datagen"):
         jobs.append((os.path.join(CSRC, name + ".cu"), os.path.join(build_dir, name + ".o"), []))
     return jobs
 
