@@ -74,8 +74,8 @@ NSW_REG(4, 128, 3)
 NSW_REG(4, 128, 4)   // 4 per SM: one wave of up to 592 users (strong-scaling shards)
 NSW_REG(8, 128, 3)
 // (tail tile capped at 128 / 80 registers to start beside draining main CTAs:
-// 0.4 / 1.2 % slower, profiles/r01g_tail_registers.txt)
-NSW_REG(8, 256, 1)   // (4, 512, 1): 16 warps, 11 % slower on config 3 (profiles/r01d_row_tiles_cfg2_cfg3.txt)
+// 0.4 / 1.2 % slower, profiles/r01/r01g_tail_registers.txt)
+NSW_REG(8, 256, 1)   // (4, 512, 1): 16 warps, 11 % slower on config 3 (profiles/r01/r01d_row_tiles_cfg2_cfg3.txt)
 NSW_REG(2, 256, 1)
 NSW_REG(1, 512, 1)
 #if NSW_EXP_TILES   // A/B builds only: 9-13-warp row tiles for config 3

@@ -43,10 +43,10 @@ NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8
 NSW_REG_CLT(13, 4, 7, 256, 9, 1)
 // (two CTAs per SM on 16-CTA clusters -- (13,4,8,128), (7,8,8,256), (13,4,4,256)
 // -- and a 14-warp (13,4,4,448) 9-CTA tile ran 3-19 % slower than the
-// 1-CTA/SM tiles: profiles/r01d_cluster_tile_variants.txt)
+// 1-CTA/SM tiles: profiles/r01/r01d_cluster_tile_variants.txt)
 // (one-CTA 2-D tiles with 16-32 warps for configs 2 / 3 -- (6,4,4,1024),
 // (11,2,4,512), (3,4,8,1024), (6,2,8,512) -- ran 9-45 % slower than the row
-// tiles: profiles/r01d_2d_tiles_cfg2_cfg3.txt)
+// tiles: profiles/r01/r01d_2d_tiles_cfg2_cfg3.txt)
 #endif
 
 }  // namespace

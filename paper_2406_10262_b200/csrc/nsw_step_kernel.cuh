@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // Packed FFMA2 in the hot loops for tiles of >= 12 warps per SM (issue-
   // bound: config 1 main wave) and the 2-row latency tiles (config-1 tail);
   // the 4- and 8-row tiles at one CTA per SM lose 5-8 % with it (configs 2,
-  // 3; profiles/r01d_ab_ffma2.txt).
+  // 3; profiles/r01/r01d_ab_ffma2.txt).
   constexpr bool PK = sizeof(S) == 4 && (NT * MINB >= 384 || R <= 2 || NSW_PK_ALL);
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
   // re-read from shared memory per row instead of held across the row loop
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // in place into padded K~ rows.
   // fp32: only the 2048-row tiles (config 3: +1.8 %); on the smaller fp32
   // tiles the extra code perturbs the hot loops' register allocation for a
-  // -0.3..-0.8 % net (profiles/r01f_ab_tma.txt).  fp64 tiles always use it.
+  // -0.3..-0.8 % net (profiles/r01/r01f_ab_tma.txt).  fp64 tiles always use it.
   constexpr bool BULK_TILE = sizeof(S) == 8 || NT * R >= 2048;
   const bool bulk = BULK_TILE && rebuild && vec_ok && !TC;
   const int stage_off = (NT * R * P - nm) / V * V;   // first staged element (16-byte aligned)
