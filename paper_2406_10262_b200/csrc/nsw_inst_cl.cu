@@ -37,6 +37,13 @@ NSW_REG_CL(2)
 NSW_REG_CL(4)
 NSW_REG_CL(8)
 NSW_REG_CL(16)   // non-portable cluster size (B200 GPCs hold 16 SMs): n up to 8192 (fp32) / 2048 (fp64)
+#if !NSW_F64 && defined(NSW_EXP_TILES) && NSW_EXP_TILES
+// A/B builds only: config 2 (1000 x 21) split over 2-CTA clusters so two
+// users share an SM (MINB 2)
+NSW_REG_CLT(21, 1, 2, 256, 2, 2)
+NSW_REG_CLT(11, 2, 4, 256, 2, 2)
+NSW_REG_CLT(21, 1, 4, 128, 2, 2)
+#endif
 #if !NSW_F64
 // 9-CTA clusters of 448 items (n <= 4032, config 4): B200's GPCs hold 15
 // resident 8- or 9-CTA clusters, so 9 x 15 = 135 SMs work instead of 120
