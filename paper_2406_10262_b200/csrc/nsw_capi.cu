@@ -727,8 +727,14 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   ALLOC(s->state, ST_WORDS * sizeof(int));
   ALLOC(s->iters, size_t(s->outer_max) * sizeof(int));
   if (generic) {
+    // CTAs of the streaming step: occupancy-bound, and their scratch (a K~
+    // and an adjoint tile each) within a quarter of the free device memory
     s->gen_ctas = gen_ctas(s->dtype, users_local);
-    ALLOC(s->gen_scratch, size_t(s->gen_ctas) * gen_scratch_elems(n, m) * es);
+    const size_t per_cta = gen_scratch_elems(n, m) * es;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && per_cta > 0)
+      s->gen_ctas = int(std::max<size_t>(1, std::min<size_t>(size_t(s->gen_ctas), free_b / 4 / per_cta)));
+    ALLOC(s->gen_scratch, size_t(s->gen_ctas) * per_cta);
   }
   if (const char* pt = std::getenv("NSW_PHASE_TIMING"); pt && *pt && *pt != '0') {
     ALLOC(s->phase_ns, size_t(users_local) * 16 * 8);
