@@ -63,11 +63,16 @@ typedef struct {
 typedef struct {
   int32_t dtype;          /* nsw_dtype: F32 throughput path, F64 parity path        */
   int32_t schedule;       /* nsw_schedule                                           */
-  int32_t device;         /* CUDA device ordinal                                    */
+  int32_t device;         /* CUDA device ordinal; -1 = the caller's current device  */
   int32_t variant;        /* -1 = automatic tile choice, else index into the table  */
   int32_t use_graph;      /* capture the outer step in a CUDA graph (1) or not (0)  */
   int32_t check_every;    /* host polls the stop flag every N outer steps           */
   int32_t tol_chunk;      /* tolerance schedule: inner iterations per forward chunk */
+  double reabsorb;        /* > 0: in-solve re-absorption -- every 8 inner iterations,
+                             once max_k |log v~_k| exceeds this many nats, the
+                             scalings are folded into K~ (beta += log v~, alpha
+                             re-normalised) and the backward crosses back; runs the
+                             streaming fused step, fixed schedule.  0 = off.       */
 } nsw_device_options;
 
 /* Returned trace; mirrors SolveTrace (reference solver.py:125-135). */

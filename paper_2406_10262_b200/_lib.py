@@ -31,7 +31,8 @@ class SolverConfigC(C.Structure):
 
 class DeviceOptionsC(C.Structure):
     _fields_ = [("dtype", C.c_int32), ("schedule", C.c_int32), ("device", C.c_int32), ("variant", C.c_int32),
-                ("use_graph", C.c_int32), ("check_every", C.c_int32), ("tol_chunk", C.c_int32)]
+                ("use_graph", C.c_int32), ("check_every", C.c_int32), ("tol_chunk", C.c_int32),
+                ("reabsorb", C.c_double)]
 
 
 class TraceC(C.Structure):

@@ -19,6 +19,9 @@
 
 #include "../../include/nswrank_b200.h"
 #include "nsw_generic.h"
+#ifndef NSW_REABS_EVERY
+#define NSW_REABS_EVERY 8
+#endif
 #include "nsw_pool.h"
 #include "nsw_registry.h"
 #include "nsw_step_kernel.cuh"
@@ -139,6 +142,10 @@ struct nsw_solver {
   bool generic = false;           // streaming fused step (no on-chip tile holds the user)
   int gen_ctas = 0;               // its CTAs (persistent over users)
   void* gen_scratch = nullptr;    // [gen_ctas][gen_scratch_elems] K~ / adjoint / row + column vectors
+  int reabs_max = 0;              // in-solve re-absorption events per user (0: off)
+  int* ev_count = nullptr;        // [U]
+  int* ev_t = nullptr;            // [U][reabs_max]
+  void* ev_ab = nullptr;          // [U][reabs_max][n + m]
   size_t smem = 0;
   const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
   size_t smem2 = 0;
@@ -220,6 +227,11 @@ void fill_step_args(nsw_solver* s, StepArgs<S>& a) {
   a.log_mass_dummy = S(std::log(double(n - m + 1)));
   a.inv_mass_dummy = S(1.0 / double(n - m + 1));
   a.phase_ns = s->phase_ns;
+  a.reabs_thr = s->reabs_max > 0 ? s->opt.reabsorb : 0.0;
+  a.reabs_max = s->reabs_max;
+  a.ev_count = s->ev_count;
+  a.ev_t = s->ev_t;
+  a.ev_ab = (S*)s->ev_ab;
 }
 
 template <typename S>
@@ -623,7 +635,10 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   }
   // no on-chip tile holds the user's n x m tile (or forced with variant -3):
   // the streaming fused step, any shape
-  const bool generic = !var || options->variant == -3;
+  const bool reabsorb = options->reabsorb > 0.0;
+  if (reabsorb && options->schedule != NSW_SCHEDULE_FIXED)
+    return fail(NSW_ERR_UNSUPPORTED, "in-solve re-absorption runs the fixed schedule");
+  const bool generic = !var || options->variant == -3 || reabsorb;
   if (generic) var = nullptr;
   // device < 0: the caller's current device
   int dev = options->device;
@@ -735,6 +750,12 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && per_cta > 0)
       s->gen_ctas = int(std::max<size_t>(1, std::min<size_t>(size_t(s->gen_ctas), free_b / 4 / per_cta)));
     ALLOC(s->gen_scratch, size_t(s->gen_ctas) * per_cta);
+  }
+  if (reabsorb) {
+    s->reabs_max = std::min((T + NSW_REABS_EVERY - 1) / NSW_REABS_EVERY, 64);
+    ALLOC(s->ev_count, size_t(users_local) * sizeof(int));
+    ALLOC(s->ev_t, size_t(users_local) * s->reabs_max * sizeof(int));
+    ALLOC(s->ev_ab, size_t(users_local) * s->reabs_max * (size_t(n) + m) * es);
   }
   if (const char* pt = std::getenv("NSW_PHASE_TIMING"); pt && *pt && *pt != '0') {
     ALLOC(s->phase_ns, size_t(users_local) * 16 * 8);
@@ -908,7 +929,7 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
                   s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->res, s->iters,
-                  s->phase_ns, s->own_tol, s->gen_scratch};
+                  s->phase_ns, s->own_tol, s->gen_scratch, s->ev_count, s->ev_t, s->ev_ab};
   if (s->stream) {
     for (void* p : bufs)
       if (p) pool_free(p, s->stream);   // back to the pool, stream-ordered

@@ -20,12 +20,16 @@
 
 namespace nsw {
 
+#ifndef NSW_REABS_EVERY
+#define NSW_REABS_EVERY 8   // inner iterations between re-absorption checks
+#endif
+
 template <typename S>
 struct GenScratch {
   S* base;        // [ctas][scratch_elems(n, m)]
   int n, m;
   __host__ __device__ static size_t elems(int n, int m) {
-    return 2 * size_t(n) * m + 4 * size_t(n) + 8 * size_t(m) + 8;
+    return 2 * size_t(n) * m + 4 * size_t(n) + 10 * size_t(m) + 8;
   }
 };
 
@@ -67,6 +71,9 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
   S* cr = v2 + m;               // [2][m] column residuals
   S* vT = cr + 2 * m;           // [m] v~^T
   S* ex = vT + m;               // [m] exposures (0 from column m-1 on)
+  S* vpc = ex + m;              // [m] v~^{t-1} in the coordinates of level t (re-absorption)
+  S* vppc = vpc + m;            // [m] v~^{t-2} likewise
+  __shared__ int ev_flag;
   // column chunks: Q row ranges per column, Q * m <= NT
   const int Q = max(1, NT / m);
   auto mass = [&](int k) -> S { return k == m - 1 ? a.mass_dummy : S(1); };
@@ -122,6 +129,11 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
     __syncthreads();
     bool forward_from_absorb = true;
     int t_start = 1;
+    // re-absorption events of the solve being differentiated (fixed schedule)
+    const bool reabs = a.reabs_max > 0 && !tolm;
+    const int nev = (reabs && (phase == PHASE_RUNNING || phase == PHASE_DONE_PENDING)) ? a.ev_count[u] : 0;
+    const int* evt = reabs ? a.ev_t + size_t(u) * a.reabs_max : nullptr;
+    const S* evab = reabs ? a.ev_ab + size_t(u) * a.reabs_max * (size_t(n) + m) : nullptr;
     if (rebuild) {
       // K~ of the solve being differentiated / continued
       for (size_t e = tid; e < nm; e += NT) {
@@ -184,11 +196,40 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
               return acc + mul_(gx_of(relu[i], ex[k], a.imp[i]), mul_(mul_(Kt[size_t(i) * m + k], sA[i]), vT[k]));
             },
             [&](int k, S tot) { v0[k] = mul_(mul_(vT[k], tot), inv_mass(k)); });
+        // lvi of the next forward, from the final coordinates (before any crossing)
+        for (int k = tid; k < m; k += NT) v2[k] = a.warm_start ? add_(v1[k], F::log_(vT[k])) : S(0);
         // ---- reverse levels t = Th..1 (sinkhorn.py:276-308), as in step_kernel
         for (int t = Th; t >= 1; --t) {
           const bool first = t == Th, last = t == 1;
           const S* vp = hu + size_t(t - 1) * m;                 // v~^{t-1}
           const S* vpp = hu + size_t(last ? 0 : t - 2) * m;     // v~^{t-2}
+          if (nev > 0) {
+            // history rows recorded before an event at t-1 / t-2 are in older
+            // coordinates than level t's: v~ / b of every event in [row, t)
+            bool cv1 = false, cv2 = false;
+            for (int e = 0; e < nev; ++e) {
+              cv1 |= evt[e] == t - 1;
+              cv2 |= !last && (evt[e] == t - 1 || evt[e] == t - 2);
+            }
+            if (cv1 || cv2) {
+              for (int k = tid; k < m; k += NT) {
+                S x1 = vp[k], x2 = last ? S(1) : vpp[k];
+                for (int e = 0; e < nev; ++e) {
+                  const S b = evab[size_t(e) * (n + m) + n + k];
+                  if (evt[e] == t - 1) {
+                    x1 = F::div(x1, b);
+                    if (!last) x2 = F::div(x2, b);
+                  }
+                  if (!last && evt[e] == t - 2) x2 = F::div(x2, b);
+                }
+                vpc[k] = x1;
+                vppc[k] = x2;
+              }
+              __syncthreads();
+              if (cv1) vp = vpc;
+              if (cv2) vpp = vppc;
+            }
+          }
           for (int i = warp; i < n; i += NW) {
             const S* row = Kt + size_t(i) * m;
             const S sig = gen_row_dot(row, v0, m, lane);
@@ -215,6 +256,29 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
                       v0[k] = mul_(mul_(vpk, gv), inv_mass(k));
                     });
           }
+          // crossing an event at t-1 (going down): back to the older coordinates,
+          // K~ / (a b'), G * (a b') (K~ .* G invariant), cv * b, u~ * a, and the
+          // seed's u~^T / v~^T likewise (they end in the first solve coordinates)
+          for (int e = 0; e < nev; ++e)
+            if (evt[e] == t - 1 && t > 1) {
+              const S* ea = evab + size_t(e) * (n + m);
+              const S* eb = ea + n;
+              for (size_t q = tid; q < nm; q += NT) {
+                const int i = int(q / m), k = int(q - size_t(i) * m);
+                const S f = mul_(ea[i], eb[k]);
+                Kt[q] = F::div(Kt[q], f);
+                G[q] = mul_(G[q], f);
+              }
+              for (int i = tid; i < n; i += NT) {
+                ut[i] = mul_(ut[i], ea[i]);
+                sA[i] = mul_(sA[i], ea[i]);
+              }
+              for (int k = tid; k < m; k += NT) {
+                v0[k] = mul_(v0[k], eb[k]);
+                vT[k] = mul_(vT[k], eb[k]);
+              }
+              __syncthreads();
+            }
         }
         // ---- gK = W + K~ .* G (into G), lvi of the next forward
         for (size_t e = tid; e < nm; e += NT) {
@@ -224,7 +288,6 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
           const S W = k < m - 1 ? mul_(gx_of(relu[i], ex[k], a.imp[i]), X) : S(0);
           G[e] = fma(kk, G[e], W);
         }
-        for (int k = tid; k < m; k += NT) v2[k] = a.warm_start ? add_(v1[k], F::log_(vT[k])) : S(0);
         __syncthreads();
         // ---- g_C = gK (-1/eps); Adam ascent (solver.py:105-122); K = C (-1/eps)
         const int s = a.state[ST_STEP];
@@ -290,6 +353,7 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
       __syncthreads();
     }
     const int t_end = tolm ? min(t_start - 1 + a.chunk, T) : T;
+    int nev_fwd = 0;
     for (int t = t_start; t <= t_end; ++t) {
       S wmax = S(0);
       for (int i = warp; i < n; i += NW) {
@@ -313,7 +377,43 @@ __global__ void __launch_bounds__(GEN_NT) step_kernel_gen(const StepArgs<S> a, c
         for (int kk = 0; kk < m; ++kk) r = fmax(r, cr[((t - 1) & 1) * m + kk]);
         a.res[size_t(u) * (T + 1) + t - 1] = double(r);
       }
+      // in-solve re-absorption: once the column scalings leave +-reabs_thr nats,
+      // fold them into K~ (beta += log v~) and re-normalise the rows (alpha += log a);
+      // v~^t stays recorded in the old coordinates, later iterations in the new
+      if (reabs && (t % NSW_REABS_EVERY) == 0 && t >= 2 && t <= T - 2 && nev_fwd < a.reabs_max) {
+        if (tid == 0) {
+          S mx = S(0);
+          for (int k = 0; k < m; ++k) mx = fmax(mx, fabs(F::log_(v0[k])));
+          ev_flag = double(mx) > a.reabs_thr;
+        }
+        __syncthreads();
+        if (ev_flag) {
+          S* ea = a.ev_ab + (size_t(u) * a.reabs_max + nev_fwd) * (size_t(n) + m);
+          for (int i = tid; i < n; i += NT) {
+            S* row = Kt + size_t(i) * m;
+            S mx = S(0);
+            for (int k = 0; k < m; ++k) {
+              row[k] = mul_(row[k], v0[k]);
+              mx = fmax(mx, row[k]);
+            }
+            const S ai = F::rcp_fast(mx);
+            for (int k = 0; k < m; ++k) row[k] = mul_(row[k], ai);
+            ea[i] = ai;
+            a.alpha[size_t(u) * n + i] = add_(a.alpha[size_t(u) * n + i], F::log_(ai));
+          }
+          __syncthreads();   // every row has used v~ before it is reset
+          for (int k = tid; k < m; k += NT) {
+            ea[n + k] = v0[k];
+            a.beta[size_t(u) * m + k] = add_(a.beta[size_t(u) * m + k], F::log_(v0[k]));
+            v0[k] = S(1);
+          }
+          if (tid == 0) a.ev_t[size_t(u) * a.reabs_max + nev_fwd] = t;
+          ++nev_fwd;
+          __syncthreads();
+        }
+      }
     }
+    if (reabs && tid == 0) a.ev_count[u] = nev_fwd;
     if (tolm) {
       S wmax = S(0);
       for (int i = warp; i < n; i += NW) {

@@ -43,6 +43,14 @@ struct StepArgs {
   S mass_dummy, log_mass_dummy;
   S inv_mass_dummy;              // 1/(n-m+1), correctly rounded on the host
   unsigned long long* phase_ns;  // [U][16] diagnostics: phase-boundary timestamps (nullptr: off)
+  // in-solve re-absorption (streaming step only; reabs_thr > 0): per user up
+  // to reabs_max events of the last forward, event e at iteration ev_t[u][e]
+  // with row factors a (n) and column factors b (m) in ev_ab[u][e][n + m]
+  double reabs_thr;
+  int reabs_max;
+  int* ev_count;   // [U]
+  int* ev_t;       // [U][reabs_max]
+  S* ev_ab;        // [U][reabs_max][n + m]
 };
 
 template <typename S>

@@ -67,6 +67,13 @@ class DeviceOptions:
     use_graph capture the outer step in a CUDA graph (fixed schedule).
     check_every  poll the device stop flag every N outer steps.
     tol_chunk inner iterations per forward launch in the tolerance schedule.
+    reabsorb  None (default) or a threshold in nats: in-solve re-absorption of
+              the Sinkhorn scalings (every 8 inner iterations, once
+              max |log v~| exceeds it, v~ is folded into K~ and alpha re-
+              normalised; the backward crosses back).  Needed only when one
+              solve's duals travel beyond the float32 exponent range (cold
+              start, warm_start=False, at small eps); runs the streaming fused
+              step, fixed schedule.
     """
 
     dtype: str = "float64"
@@ -76,6 +83,7 @@ class DeviceOptions:
     use_graph: bool = True
     check_every: int = 16
     tol_chunk: int = 16
+    reabsorb: float | None = None
 
     def to_c(self) -> _lib.DeviceOptionsC:
         if self.dtype not in ("float32", "float64"):
@@ -86,7 +94,7 @@ class DeviceOptions:
             _lib.NSW_F64 if self.dtype == "float64" else _lib.NSW_F32,
             _lib.NSW_SCHEDULE_FIXED if self.schedule == "fixed" else _lib.NSW_SCHEDULE_TOLERANCE,
             -1 if self.device is None else int(self.device), int(self.variant), int(bool(self.use_graph)), int(self.check_every),
-            int(self.tol_chunk))
+            int(self.tol_chunk), float(self.reabsorb or 0.0))
 
 
 def _config_c(cfg) -> _lib.SolverConfigC:
