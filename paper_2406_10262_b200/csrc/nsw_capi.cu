@@ -867,12 +867,33 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
       }
     }
   }
-  // inputs
-  if ((e = s->dtype == NSW_F64 ? upload_converted<double>(s->rel, relevance_local, size_t(users_local) * n)
-                              : upload_converted<float>(s->rel, relevance_local, size_t(users_local) * n)) !=
-      NSW_OK) {
-    nsw_solver_destroy(s);
-    return e;
+  // inputs: the float64 relevance goes to the device as is; the fp32 copy
+  // and sum_u r^2 (when the caller does not pass it) are formed there
+  {
+    const size_t cells_r = size_t(users_local) * n;
+    double* r64 = nullptr;
+    if (s->dtype == NSW_F64) {
+      r64 = static_cast<double*>(s->rel);
+    } else if ((e = pool_malloc((void**)&r64, cells_r * 8, s->stream)) != NSW_OK ||
+               cudaStreamSynchronize(s->stream) != cudaSuccess) {
+      nsw_solver_destroy(s);
+      return e != NSW_OK ? e : fail(NSW_ERR_CUDA, "relevance staging failed");
+    }
+    cudaError_t ce = cudaMemcpyAsync(r64, relevance_local, cells_r * 8, cudaMemcpyHostToDevice, s->stream);
+    if (ce == cudaSuccess && s->dtype == NSW_F32) {
+      narrow_kernel<<<sm_count() * 4, 256, 0, s->stream>>>(r64, static_cast<float*>(s->rel), cells_r);
+      ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess && !rel_sq_sum) {
+      rel_sq_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(r64, users_local, n, s->rel_sq);
+      ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s->stream);
+    if (s->dtype == NSW_F32) pool_free(r64, s->stream);
+    if (ce != cudaSuccess) {
+      nsw_solver_destroy(s);
+      return fail(NSW_ERR_CUDA, std::string("relevance upload: ") + cudaGetErrorString(ce));
+    }
   }
   s->expo_host.assign(exposure, exposure + (m - 1));
   std::vector<double> ex(m, 0.0);
@@ -886,13 +907,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return e;
   }
-  std::vector<double> rsq(n, 0.0);
-  if (rel_sq_sum) {
-    for (int i = 0; i < n; ++i) rsq[i] = rel_sq_sum[i];
-  } else {
-    for (int u = 0; u < users_local; ++u)
-      for (int i = 0; i < n; ++i) rsq[i] += relevance_local[size_t(u) * n + i] * relevance_local[size_t(u) * n + i];
-  }
+
   // Adam bias corrections exactly as the reference computes them (Python
   // floats: 1.0 - b1**step, solver.py:118-119).
   std::vector<double> bc(size_t(2) * (s->outer_max + 1), 1.0);
@@ -903,7 +918,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   const double neg_inf = -INFINITY;
   int init_state[ST_WORDS] = {PHASE_INIT, 0, 0, 0, 0, 0, 0, 0};
   if (cudaMemcpy(s->expo_d, ex.data(), m * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(s->rel_sq, rsq.data(), n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+      (rel_sq_sum && cudaMemcpy(s->rel_sq, rel_sq_sum, n * 8, cudaMemcpyHostToDevice) != cudaSuccess) ||
       cudaMemcpy(s->bc, bc.data(), bc.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(s->best, &neg_inf, 8, cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaMemcpy(s->state, init_state, sizeof(init_state), cudaMemcpyHostToDevice) != cudaSuccess) {

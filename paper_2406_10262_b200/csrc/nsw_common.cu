@@ -242,6 +242,26 @@ __global__ void flush_kernel(float* buf, size_t n) {
     buf[i] = buf[i] * 0.5f + 1.0f;
 }
 
+// float64 -> float32 (round to nearest, as the host's float(x))
+__global__ void narrow_kernel(const double* __restrict__ src, float* __restrict__ dst, size_t n) {
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    dst[i] = __double2float_rn(src[i]);
+}
+
+// rsq_i = sum_u r_ui^2 in user order with separate multiply / add roundings
+// (the closed-form gradient norm's item weights, solver.py:211)
+__global__ void rel_sq_kernel(const double* __restrict__ rel, int U, int n, double* __restrict__ rsq) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double acc = 0.0;
+#pragma unroll 8
+  for (int u = 0; u < U; ++u) {
+    const double r = rel[size_t(u) * n + i];
+    acc = __dadd_rn(acc, __dmul_rn(r, r));
+  }
+  rsq[i] = acc;
+}
+
 __global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, size_t n, unsigned* bad) {
   bool ok = true;
   for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {

@@ -1221,5 +1221,7 @@ __global__ void stamp_kernel(unsigned long long* stamp);
 __global__ void flush_kernel(float* buf, size_t n);
 __global__ void discard_kernel(float* buf, size_t n);
 __global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, size_t n, unsigned* bad);
+__global__ void narrow_kernel(const double* __restrict__ src, float* __restrict__ dst, size_t n);
+__global__ void rel_sq_kernel(const double* __restrict__ rel, int U, int n, double* __restrict__ rsq);
 
 }  // namespace nsw
