@@ -173,6 +173,8 @@ struct nsw_solver {
   std::vector<double> expo_host;     // exposures [m-1] (metrics)
   cudaStream_t stream = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraphExec_t tol_gexec = nullptr;   // tolerance schedule, single shard: one graph per outer step
+  cudaStream_t body_stream = nullptr;    // capture stream of its while-loop body
   bool graph_dirty = true;
   int64_t launches = 0;
   StepArgs<float> a32{}, b32{};   // main / tail launch arguments
@@ -941,6 +943,8 @@ nsw_status nsw_solver_destroy(nsw_solver* s) {
   if (!s) return NSW_OK;
   DeviceGuard guard(s->device);
   if (s->gexec) cudaGraphExecDestroy(s->gexec);
+  if (s->tol_gexec) cudaGraphExecDestroy(s->tol_gexec);
+  if (s->body_stream) cudaStreamDestroy(s->body_stream);
   void* bufs[] = {s->C, s->am, s->av, s->alpha, s->beta, s->hist, s->xbest, s->rel, s->expo, s->expo_d,
                   s->partial, s->split, s->own_imp_local, s->own_imp_all, s->imp_cur, s->rel_sq, s->best,
                   s->objective, s->grad_norm, s->bc, s->stamp, s->counter, s->state, s->res, s->iters,
@@ -1051,6 +1055,73 @@ static nsw_status tol_local(nsw_solver* s, cudaStream_t st) {
   return NSW_OK;
 }
 
+// Single-shard tolerance schedule as ONE graph per outer step, no host
+// round trip per chunk: [fused launch] -> while (cond) { chunk maxima ->
+// decide (sets cond = another chunk follows) -> fused launch (next chunk, or
+// the finish launch once t* is known) } -> impact reduction + finalize.
+static nsw_status ensure_tol_graph(nsw_solver* s) {
+  if (s->tol_gexec && !s->graph_dirty) return NSW_OK;
+  if (s->tol_gexec) {
+    cudaGraphExecDestroy(s->tol_gexec);
+    s->tol_gexec = nullptr;
+  }
+  if (!s->body_stream) CUDA_TRY(cudaStreamCreateWithFlags(&s->body_stream, cudaStreamNonBlocking));
+  const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
+  const int64_t before = s->launches;
+  cudaStream_t st = s->stream;
+  CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  nsw_status e = launch_fused(s, st);
+  cudaGraph_t capg = nullptr, g = nullptr;
+  cudaGraphNode_t cnode = nullptr;
+  cudaGraphConditionalHandle h = 0;
+  cudaError_t ce = cudaSuccess;
+  if (e == NSW_OK) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &capg, &deps, &ndeps);
+    if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&h, capg, 1, cudaGraphCondAssignDefault);
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    if (ce == cudaSuccess) ce = cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp);
+    if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies);
+    if (ce == cudaSuccess) {
+      cudaGraph_t body = cp.conditional.phGraph_out[0];
+      ce = cudaStreamBeginCaptureToGraph(s->body_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+      if (ce == cudaSuccess) {
+        tol_chunk_max_kernel<<<1, 256, 0, s->body_stream>>>(s->res, s->U, s->T, chunk, s->state, s->tolbuf);
+        tol_decide_kernel<<<1, 32, 0, s->body_stream>>>(s->tolbuf, s->T, chunk, s->cfg.sinkhorn_tol, s->state,
+                                                         static_cast<unsigned long long>(h));
+        e = launch_fused(s, s->body_stream);
+        cudaGraph_t bg = nullptr;
+        const cudaError_t ce2 = cudaStreamEndCapture(s->body_stream, &bg);
+        if (ce == cudaSuccess) ce = ce2;
+      }
+    }
+  }
+  if (e == NSW_OK && ce == cudaSuccess) e = launch_impact_reduce(s, st, true);
+  const cudaError_t ce3 = cudaStreamEndCapture(st, &g);
+  s->launches = before;
+  if (e != NSW_OK) {
+    if (g) cudaGraphDestroy(g);
+    return e;
+  }
+  if (ce != cudaSuccess || ce3 != cudaSuccess) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    return fail(NSW_ERR_CUDA, std::string("tolerance graph capture: ") +
+                                  cudaGetErrorString(ce != cudaSuccess ? ce : ce3));
+  }
+  ce = cudaGraphInstantiate(&s->tol_gexec, g, 0);
+  cudaGraphDestroy(g);
+  if (ce != cudaSuccess) return fail(NSW_ERR_CUDA, std::string("tolerance graph instantiate: ") + cudaGetErrorString(ce));
+  s->graph_dirty = false;
+  return NSW_OK;
+}
+
 static nsw_status tol_decide(nsw_solver* s, cudaStream_t st, int* phase) {
   const int chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
   tol_decide_kernel<<<1, 32, 0, st>>>(s->tolbuf, s->T, chunk, s->cfg.sinkhorn_tol, s->state);
@@ -1063,6 +1134,13 @@ static nsw_status tol_decide(nsw_solver* s, cudaStream_t st, int* phase) {
 }
 
 static nsw_status one_step_tolerance(nsw_solver* s) {
+  if (s->opt.use_graph && fuse_finalize(s)) {
+    nsw_status ge = ensure_tol_graph(s);
+    if (ge != NSW_OK) return ge;
+    CUDA_TRY(cudaGraphLaunch(s->tol_gexec, s->stream));
+    s->launches += 4;   // at least: fused, chunk maxima, decide, finish + impact reduction (data-dependent)
+    return NSW_OK;
+  }
   nsw_status e = launch_fused(s, s->stream);
   if (e != NSW_OK) return e;
   for (;;) {

@@ -121,10 +121,16 @@ __global__ void __launch_bounds__(256) tol_chunk_max_kernel(const double* __rest
   }
 }
 
-__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state) {
-  const int phase = state[ST_PHASE];
-  if (!(phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME || phase == PHASE_FWD_CONT)) return;
+// cond (nonzero): the while-conditional of the single-shard tolerance graph,
+// set to "another forward chunk follows" in every path
+__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state,
+                                  unsigned long long cond) {
   if (threadIdx.x != 0) return;
+  const int phase = state[ST_PHASE];
+  if (!(phase == PHASE_INIT || phase == PHASE_RUNNING || phase == PHASE_RESUME || phase == PHASE_FWD_CONT)) {
+    if (cond) cudaGraphSetConditional(cond, 0u);
+    return;
+  }
   const int t0 = state[ST_T0];
   const int t1 = min(t0 + chunk, T);
   int tstar = 0;
@@ -140,6 +146,7 @@ __global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int ch
     state[ST_T0] = t1;
     state[ST_PHASE] = PHASE_FWD_CONT;
   }
+  if (cond) cudaGraphSetConditional(cond, state[ST_PHASE] == PHASE_FWD_CONT ? 1u : 0u);
 }
 
 // Objective, gradient norm, trace, best iterate, stop and error decisions

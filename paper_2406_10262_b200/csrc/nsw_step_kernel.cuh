@@ -1213,7 +1213,8 @@ __global__ void impact_reduce_kernel(const double* __restrict__ partial, int U, 
 //     sets PHASE_FWD_FIN (t* found or the budget is spent) or PHASE_FWD_CONT.
 __global__ void tol_chunk_max_kernel(const double* __restrict__ res, int U, int T, int chunk, const int* state,
                                      double* __restrict__ cmax);
-__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state);
+__global__ void tol_decide_kernel(const double* __restrict__ cmax, int T, int chunk, double tol, int* state,
+                                  unsigned long long cond = 0);
 
 
 __global__ void finalize_kernel(FinalizeArgs f);

@@ -28,16 +28,18 @@ def main():
         U, n = rel.shape
         cfg = SolverConfig(epsilon=eps, sinkhorn_tol=1e-6 if dtype == "float64" else 1e-5, outer_max_iters=25)
         args = (RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, expo.size + 1), cfg)
-        t0 = time.perf_counter()
-        try:
-            pol, tr = solve_fair_ranking(*args, DeviceOptions(dtype=dtype, schedule="tolerance", tol_chunk=chunk))
-        except SolverError as e:
-            tr = e.trace
-        dt = time.perf_counter() - t0
-        its = tr.sinkhorn_iterations
-        print(f"chunk {chunk} {name} U={U} {dtype}: {len(tr)} steps in {dt*1e3:.1f} ms ({dt/len(tr)*1e3:.2f} ms/step), "
-              f"inner iterations {its[:3]}..{its[-3:]} total {sum(its)}, "
-              f"{sum(its)/dt:.0f} inner it/s")
+        for graph in (False, True, False, True):
+            t0 = time.perf_counter()
+            try:
+                pol, tr = solve_fair_ranking(*args, DeviceOptions(dtype=dtype, schedule="tolerance", tol_chunk=chunk,
+                                                                  use_graph=graph))
+            except SolverError as e:
+                tr = e.trace
+            dt = time.perf_counter() - t0
+            its = tr.sinkhorn_iterations
+            print(f"chunk {chunk} {name} U={U} {dtype} {'device-driven graph' if graph else 'host-driven chunks'}: "
+                  f"{len(tr)} steps in {dt*1e3:.1f} ms ({dt/len(tr)*1e3:.2f} ms/step), "
+                  f"inner iterations {its[:3]}..{its[-3:]} total {sum(its)}, {sum(its)/dt:.0f} inner it/s")
 
 
 if __name__ == "__main__":
