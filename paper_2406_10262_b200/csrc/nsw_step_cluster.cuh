@@ -478,6 +478,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       }
       reduce_cols(c, [&](int k, S tot) { vec0[k] = mul_(mul_(vTr[k], tot), inv_mass(k)); });
     }
+#ifndef NSW_KREG_CL
+#define NSW_KREG_CL 1   // +1.5 % on the config-4 shard (profiles/r02/ab_kreg_cluster.txt)
+#endif
+    // KREG: the K~ row segments stay in registers for the whole sweep
+    constexpr bool KREG = NSW_KREG_CL && sizeof(S) == 4 && R <= 7;   // R = 8 tiles would spill
+    S Kr[KREG ? R : 1][MC];
+    if constexpr (KREG) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) ld_seg<Tl, S, MC>(Kr[r], Kt, lrow(r), g);
+    }
     for (int t = Th; t >= 1; --t) {
       // stream row t-3 into the slot row t+1 held (last read at level t+2)
       if (t >= 3) load_row(vrow(t - 3), t - 3);
@@ -496,7 +506,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);
         S kr[MC];
-        ld_seg<Tl, S, MC>(kr, Kt, il, g);
+        if constexpr (KREG) {
+#pragma unroll
+          for (int j = 0; j < MC; ++j) kr[j] = Kr[r][j];
+        } else {
+          ld_seg<Tl, S, MC>(kr, Kt, il, g);
+        }
         const S sig = rdot_g<S, MC, CG>(kr, cv);
         const S den = rdot_g<S, MC, CG>(kr, vpp);
         const S gs = first ? rowB[il] : S(0);

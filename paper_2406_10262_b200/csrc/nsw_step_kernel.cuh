@@ -795,6 +795,23 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       // the previous level's broadcast reduction (NSW_BCAST) or from vec0
       S cvr[M];
       if constexpr (NSW_BCAST) lds_vec<S, M>(cvr, vec0);
+      // KREG: the K~ rows stay in registers for the whole sweep
+      // (next to the adjoint) instead of one shared-memory row read per level
+#ifndef NSW_KREG_BWD
+#define NSW_KREG_BWD 1   // +12 % config 2, +3 % config 3 (profiles/r02/ab_kreg_backward.txt)
+#endif
+#ifndef NSW_KREG_MINR
+#define NSW_KREG_MINR 2   // R = 2 tail tiles: +2.7 % config 1 (profiles/r02/ab_kreg_tail_tiles.txt)
+#endif
+      // (only where the two R x M tiles and the level vectors fit the register cap)
+      constexpr int REG_CAP = (65536 / (NT * MINB)) < 255 ? (65536 / (NT * MINB)) : 255;
+      constexpr bool KREG = NSW_KREG_BWD && sizeof(S) == 4 && MINB == 1 && R >= NSW_KREG_MINR &&
+                            2 * R * M + 3 * M + 24 <= REG_CAP;
+      S Kr[KREG ? R : 1][M];
+      if constexpr (KREG) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) lds_vec<S, M>(Kr[r], Kt + size_t(tid + r * NT) * P);
+      }
       auto level = [&](const int t, auto first_c, auto last_c) {
         constexpr bool FIRST = decltype(first_c)::value;
         constexpr bool LAST = decltype(last_c)::value;
@@ -814,7 +831,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         for (int r = 0; r < R; ++r) {
           const int i = tid + r * NT;
           S kr[M];
-          lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          if constexpr (KREG) {
+#pragma unroll
+            for (int k = 0; k < M; ++k) kr[k] = Kr[r][k];
+          } else {
+            lds_vec<S, M>(kr, Kt + size_t(i) * P);
+          }
           const S sig = rdot<S, M, CH, PK>(kr, cv);
           S den = S(1);
           if constexpr (!LAST) {
