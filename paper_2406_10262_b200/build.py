@@ -77,19 +77,36 @@ def _compile(job, force, verbose, defines=()):
 
 
 def build(jobs: int | None = None, force: bool = False, verbose: bool = False, tag: str = "",
-          defines: tuple = ()) -> str:
+          defines: tuple = (), only: tuple = ()) -> str:
     """Build the library; `tag` + `defines` make an A/B variant
-    (libnswrank_b200_<tag>.so, loaded via NSW_LIB_PATH) for experiments."""
+    (libnswrank_b200_<tag>.so, loaded via NSW_LIB_PATH) for experiments.
+    `only` (A/B variants): object names (e.g. inst_f32_M21) compiled with the
+    defines; every other object is taken from the default build."""
     build_dir = BUILD if not tag else os.path.join(os.environ.get("TMPDIR", "/tmp"), f"nswrank_b200_build_{tag}")
     lib = LIB if not tag else os.path.join(HERE, f"libnswrank_b200_{tag}.so")
     os.makedirs(build_dir, exist_ok=True)
     work = _jobs(build_dir)
+    if only:
+        if not tag:
+            raise ValueError("only= builds an A/B variant: give it a tag")
+        keep = []
+        for src, obj, extra in work:
+            name = os.path.splitext(os.path.basename(obj))[0]
+            if name in only:
+                keep.append((src, obj, extra))
+            else:
+                base = os.path.join(BUILD, os.path.basename(obj))
+                if not os.path.exists(base):
+                    raise RuntimeError(f"{base} missing: run the default build first")
+                shutil.copy2(base, obj)
+                os.utime(obj)
+        work_all, work = work, keep
     n = jobs or max(1, min(len(work), os.cpu_count() or 4))
     logs = []
     with cf.ThreadPoolExecutor(max_workers=n) as ex:
         for obj, status, log in ex.map(lambda j: _compile(j, force, verbose, defines), work):
             logs.append((obj, status, log))
-    objs = [o for o, _, _ in logs]
+    objs = [o for _, o, _ in (work_all if only else work)]
     newest = max(os.path.getmtime(o) for o in objs)
     if force or not os.path.exists(lib) or os.path.getmtime(lib) < newest:
         tmp = lib + ".tmp"
@@ -112,8 +129,9 @@ def main(argv=None):
     ap.add_argument("-v", action="store_true")
     ap.add_argument("--tag", default="", help="A/B variant name (libnswrank_b200_<tag>.so)")
     ap.add_argument("-D", dest="defines", action="append", default=[], help="extra preprocessor definition")
+    ap.add_argument("--only", default="", help="comma list of objects to compile for an A/B variant (rest: default build)")
     a = ap.parse_args(argv)
-    print(build(a.j, a.force, a.v, a.tag, tuple(a.defines)))
+    print(build(a.j, a.force, a.v, a.tag, tuple(a.defines), tuple(x for x in a.only.split(",") if x)))
 
 
 if __name__ == "__main__":

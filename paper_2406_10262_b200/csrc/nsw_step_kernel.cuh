@@ -236,6 +236,16 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // the 4- and 8-row tiles at one CTA per SM lose 5-8 % with it (configs 2,
   // 3; profiles/r01/r01d_ab_ffma2.txt).
   constexpr bool PK = sizeof(S) == 4 && (NT * MINB >= 384 || R <= 2 || NSW_PK_ALL);
+  // the row dot's form (forward, replay and u~^T share it, so replays are
+  // bit-exact) and the forward's column axpy, separately
+#ifndef NSW_PK_DOT
+#define NSW_PK_DOT 0
+#endif
+#ifndef NSW_PK_FWD_AXPY
+#define NSW_PK_FWD_AXPY 0
+#endif
+  constexpr bool PKD = PK || (NSW_PK_DOT && sizeof(S) == 4);
+  constexpr bool PKF = PK || (NSW_PK_FWD_AXPY && sizeof(S) == 4);
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
   // re-read from shared memory per row instead of held across the row loop
   constexpr bool LEAN = MINB >= 7;
@@ -493,7 +503,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       for (int i = tid; i < NT * R; i += NT) {
         S kr[M];
         lds_vec<S, M>(kr, Kt + size_t(i) * P);
-        slotA(i) = i < n ? F::rcp_fast(rdot<S, M, CH, PK>(kr, vT1)) : S(0);   // u~^T
+        slotA(i) = i < n ? F::rcp_fast(rdot<S, M, CH, PKD>(kr, vT1)) : S(0);   // u~^T
       }
     }
     const int improved = a.state[ST_IMPROVED];
@@ -632,7 +642,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
         for (int r = 0; r < R; ++r) {
           const int i = tid + r * NT;
           const S sig = rdot<S, M, CH, PK>(Kr[r], cv);
-          const S den = rdot<S, M, CH, PK>(Kr[r], vpp);
+          const S den = rdot<S, M, CH, PKD>(Kr[r], vpp);
           S gs = S(0);
           if (first) {
             gs = slotB(i);
@@ -807,6 +817,22 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       constexpr int REG_CAP = (65536 / (NT * MINB)) < 255 ? (65536 / (NT * MINB)) : 255;
       constexpr bool KREG = NSW_KREG_BWD && sizeof(S) == 4 && MINB == 1 && R >= NSW_KREG_MINR &&
                             2 * R * M + 3 * M + 24 <= REG_CAP;
+      // packed FFMA2 (fma.rn.f32x2) in the register-resident backward's sig
+      // dot and rank-1 updates: its issue rate is bound by register-bank reads
+      // (a 3-register FFMA needs two cycles unless an operand comes from the
+      // reuse cache), and a packed FMA with a broadcast operand halves the
+      // instructions for the same reads
+#ifndef NSW_PK_BWD
+#define NSW_PK_BWD 1
+#endif
+      constexpr bool PKB = PK || (NSW_PK_BWD && sizeof(S) == 4 && KREG);
+      // the replay dot packed too (backward -5 %, config 2): fp32 replays then
+      // differ from the forward's u~ in the last bits (fp64 never packs); the
+      // forward's own dot stays scalar (packed it is 10 % slower: latency-bound)
+#ifndef NSW_PK_REPLAY
+#define NSW_PK_REPLAY 1
+#endif
+      constexpr bool PKR = PKD || (NSW_PK_REPLAY && PKB);
       S Kr[KREG ? R : 1][M];
       if constexpr (KREG) {
 #pragma unroll
@@ -837,19 +863,19 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           } else {
             lds_vec<S, M>(kr, Kt + size_t(i) * P);
           }
-          const S sig = rdot<S, M, CH, PK>(kr, cv);
+          const S sig = rdot<S, M, CH, PKB>(kr, cv);
           S den = S(1);
           if constexpr (!LAST) {
             S vpp[M];
             if constexpr (LEAN) lds_vec_nc<S, M>(vpp, vppp);
             else lds_vec<S, M>(vpp, vppp);
-            den = rdot<S, M, CH, PK>(kr, vpp);
+            den = rdot<S, M, CH, PKR>(kr, vpp);
           }
           const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
           if constexpr (LEAN) lds_vec_nc<S, M>(vp, vpp1);
-          axpy_<S, M, PK>(A[r], cv, -ut[r]);
-          axpy_<S, M, PK>(A[r], vp, -h);
-          if constexpr (!LAST) axpy_<S, M, PK>(c, kr, h);
+          axpy_<S, M, PKB>(A[r], cv, -ut[r]);
+          axpy_<S, M, PKB>(A[r], vp, -h);
+          if constexpr (!LAST) axpy_<S, M, PKB>(c, kr, h);
           if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
         if constexpr (!LAST) {
@@ -1087,11 +1113,11 @@ forward_iterations:
         for (int t = t_start; t <= t_end; ++t) {
           S c[M];
 #pragma unroll
-          for (int r = 0; r < R; ++r) ut[r] = rcp_clamped(rdot<S, M, CH, PK>(A[r], vv));
+          for (int r = 0; r < R; ++r) ut[r] = rcp_clamped(rdot<S, M, CH, PKD>(A[r], vv));
 #pragma unroll
           for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
-          for (int r = 0; r < R; ++r) axpy_<S, M, PK>(c, A[r], ut[r]);
+          for (int r = 0; r < R; ++r) axpy_<S, M, PKF>(c, A[r], ut[r]);
           cta_reduce_cols_bcast<S, M, NT>(
               c, red + (t & 1) * NW * M, m,
               [&](int k, S tot) -> S {
@@ -1113,7 +1139,7 @@ forward_iterations:
         S rmax = S(0);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const S sr = rdot<S, M, CH, PK>(A[r], vv);
+          const S sr = rdot<S, M, CH, PKD>(A[r], vv);
           if (TOLM && ok(r)) rmax = fmax(rmax, fabs(ut[r] * sr - S(1)));
           ut[r] = rcp_clamped(sr);
         }
@@ -1124,7 +1150,7 @@ forward_iterations:
 #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
 #pragma unroll
-        for (int r = 0; r < R; ++r) axpy_<S, M, PK>(c, A[r], ut[r]);
+        for (int r = 0; r < R; ++r) axpy_<S, M, PKF>(c, A[r], ut[r]);
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
           const S vn = F::div_fast(mass(k), tot);
           vec0[k] = vn;
@@ -1157,7 +1183,7 @@ forward_iterations:
       S rmax = S(0);
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M, CH, PK>(A[r], vv) - S(1)));
+        if (ok(r)) rmax = fmax(rmax, fabs(ut[r] * rdot<S, M, CH, PKD>(A[r], vv) - S(1)));
       rmax = warp_max(rmax);
       if (lane == 0) redmax[warp] = rmax;
       __syncthreads();
