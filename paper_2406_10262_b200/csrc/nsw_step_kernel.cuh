@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
       pf(vu, size_t(nm) * sizeof(S));
     }
   }
+
   // zero the tile (padding rows / columns must stay 0) and the small vectors;
   // a bulk-copied tile is rebuilt as whole padded rows instead
   if (!bulk)
