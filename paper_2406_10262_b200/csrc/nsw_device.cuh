@@ -275,6 +275,37 @@ __device__ __forceinline__ void cta_reduce_cols(S (&v)[M], S* red, int m, Fin fi
   __syncthreads();
 }
 
+// The same column reduction over the first NTA threads of the CTA only
+// (named barrier 1): the forward of the wide-row tiles runs on half the warps.
+template <int NTA>
+__device__ __forceinline__ void bar_part() {
+  asm volatile("bar.sync 1, %0;" ::"n"(NTA) : "memory");
+}
+template <typename S, int M, int NTA, class Op, class Fin>
+__device__ __forceinline__ void cta_reduce_cols_part(S (&v)[M], S* red, int m, Fin fin) {
+  constexpr int NW = NTA / 32;
+  constexpr int CF = (M + 31) / 32;
+  int lane;
+  asm volatile("mov.u32 %0, %%laneid;" : "=r"(lane));
+  const int warp = threadIdx.x >> 5;
+  int base = 0, lim = M;
+  reduce_scatter<S, M, M, 16, Op>(v, lane, base, lim);
+#pragma unroll
+  for (int j = 0; j < CF; ++j) {
+    const int col = base + j;
+    if (col < lim && col < m) red[warp * M + col] = v[j];
+  }
+  bar_part<NTA>();
+  if (threadIdx.x < m) {
+    const int k = threadIdx.x;
+    S acc = red[k];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) acc = Op{}(acc, red[w * M + k]);
+    fin(k, acc);
+  }
+  bar_part<NTA>();
+}
+
 // Same reduction with the finished vector delivered to EVERY thread in
 // registers (M <= 32): after the warp reduce-scatter and one barrier, every
 // warp sums the per-warp partials in warp order itself (lane k: column k) and

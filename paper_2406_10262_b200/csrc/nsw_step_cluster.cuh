@@ -261,7 +261,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   // of every CTA (identical bits everywhere)
   // xval: this CTA's row-residual max (tolerance mode) travels in slot m of
   // the exchange; the cluster maximum is returned in *xmax on thread m
-  auto reduce_cols = [&](S (&v)[MC], auto&& fin, bool xon = false, S xval = S(0), S* xmax = nullptr) {
+  // split in two so independent work can run while the exchange is in
+  // flight: post_cols (partials -> barrier -> warp sums -> DSMEM pushes) and
+  // collect_cols (wait for every rank's totals -> fin -> barrier)
+  auto post_cols = [&](S (&v)[MC], bool xon = false, S xval = S(0)) {
     int base = 0, lim = MC;
     rs_rows<S, MC, MC, 16, CG, OpSum>(v, lane, base, lim);
     constexpr int CF = rs_final_count<MC, 16, CG>();
@@ -300,6 +303,12 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
 #pragma unroll
         for (int q = 0; q < CL; ++q) cl_st_async16(cl_map(slot, q), mine, cl_map(mb, q));
       }
+    }
+  };
+  auto collect_cols = [&](auto&& fin, bool xon = false, S xval = S(0), S* xmax = nullptr) {
+    if constexpr (CL > 1) {
+      const uint32_t mb = smem_u32(xmb + parity);
+      const int nx = m + (xon ? 1 : 0);
       if (tid < nx) {
         mbar_wait(mb, (xph >> parity) & 1u);
         if (tid < m) {
@@ -327,6 +336,10 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       if (xon && tid == m) *xmax = xval;
     }
     __syncthreads();
+  };
+  auto reduce_cols = [&](S (&v)[MC], auto&& fin, bool xon = false, S xval = S(0), S* xmax = nullptr) {
+    post_cols(v, xon, xval);
+    collect_cols(fin, xon, xval, xmax);
   };
   // v~ history rows: global (written by the forward) -> shared slots by
   // cp.async, zero-filled past column m-1
@@ -494,6 +507,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       S cv[MC], vp[MC], vpp[MC], c[MC];
       const S* rp = vrow(t - 1);
       const S* rpp = vrow(t >= 2 ? t - 2 : 0);
+      const bool first = t == Th;
 #pragma unroll
       for (int j = 0; j < MC; ++j) {
         cv[j] = vec0[col(j)];
@@ -501,7 +515,6 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
         vpp[j] = rpp[col(j)];
         c[j] = S(0);
       }
-      const bool first = t == Th;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int il = lrow(r);

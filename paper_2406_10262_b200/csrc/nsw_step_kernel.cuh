@@ -1083,6 +1083,59 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   __syncthreads();
   mark(9);
 forward_iterations:
+  // Wide-row forward (fixed schedule, one-CTA-per-SM fp32 tiles whose
+  // doubled row tile fits the register file): half the warps each hold 2R
+  // K~ rows; the column reduction's shuffle and barrier work is per warp, so
+  // it halves, and the rows supply the FMA chains' independence (config 2:
+  // the reduce-scatter and its barriers were ~40 % of the forward).
+#ifndef NSW_WIDE_FWD
+#define NSW_WIDE_FWD 1
+#endif
+  if constexpr (NSW_WIDE_FWD && sizeof(S) == 4 && MINB == 1 && NT >= 256 && R <= 4 && M <= 32 && !TC &&
+                2 * R * M + 2 * M + 2 * R + 24 <= (65536 / NT < 255 ? 65536 / NT : 255)) {
+    if (!tolm) {
+      constexpr int NTA = NT / 2, RA = 2 * R;
+      if (tid >= NTA) return;   // nothing after the forward needs the idle warps
+      S A[RA][M];
+      S ut[RA];
+#pragma unroll
+      for (int r = 0; r < RA; ++r) lds_vec<S, M>(A[r], Kt + size_t(tid + r * NTA) * P);
+      S vv[M];
+      for (int t = 1; t <= T; ++t) {
+        lds_vec<S, M>(vv, vec0);
+        S c[M];
+#pragma unroll
+        for (int r = 0; r < RA; ++r) ut[r] = rcp_clamped(rdot<S, M, 1, PKD>(A[r], vv));
+#pragma unroll
+        for (int k = 0; k < M; ++k) c[k] = S(0);
+#pragma unroll
+        for (int r = 0; r < RA; ++r) axpy_<S, M, PKF>(c, A[r], ut[r]);
+        cta_reduce_cols_part<S, M, NTA, OpSum>(c, red, m, [&](int k, S tot) {
+          const S vn = F::div_fast(mass(k), tot);
+          vec0[k] = vn;
+          hu[size_t(t) * m + k] = vn;
+        });
+      }
+      mark(10);
+      lds_vec<S, M>(vv, vec0);
+#pragma unroll
+      for (int r = 0; r < RA; ++r) {
+        const int i = tid + r * NTA;
+        const double rr = double(rel_of(i));
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+          if (k < m - 1) {
+            const S X = mul_(mul_(A[r][k], ut[r]), vv[k]);
+            acc = fma(rr * exD[k], double(X), acc);
+          }
+        }
+        if (i < n) a.partial[size_t(u) * n + i] = acc;
+      }
+      mark(11);
+      return;
+    }
+  }
   {
     S A[R][M];  // K~, register resident
     S ut[R];
