@@ -21,7 +21,7 @@ minf = int(sys.argv[2])
 W = int(sys.argv[3]) if len(sys.argv) > 3 else 40
 loops = []
 for i, (a, s, _) in enumerate(ins):
-    m = re.search(r"BRA (?:`\(\.L_x_\d+\) )?0x([0-9a-f]+)", s)
+    m = re.search(r"BRA(?:\.\w+)*\s+(?:!?U?P\w+,\s*)?(?:`\(\.L_x_\d+\)\s*)?0x([0-9a-f]+)", s)
     if m:
         t = int(m.group(1), 16)
         if t <= a and t in addr:

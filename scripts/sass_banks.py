@@ -23,7 +23,7 @@ for f in re.split(r"\n\s*Function : ", out):
             ins.append((int(m.group(1), 16), m.group(2).strip()))
     addr = {a: i for i, (a, _) in enumerate(ins)}
     for i, (a, t) in enumerate(ins):
-        m = re.search(r"BRA (?:`\(\.L_x_\d+\) )?0x([0-9a-f]+)", t)
+        m = re.search(r"BRA(?:\.\w+)*\s+(?:!?U?P\w+,\s*)?(?:`\(\.L_x_\d+\)\s*)?0x([0-9a-f]+)", t)
         if not (m and int(m.group(1), 16) <= a and int(m.group(1), 16) in addr):
             continue
         body = ins[addr[int(m.group(1), 16)]:i + 1]

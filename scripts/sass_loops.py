@@ -22,7 +22,7 @@ for f in funcs:
     addr = {a: i for i, (a, _) in enumerate(ins)}
     print("==", name[:110], len(ins), "instructions")
     for i, (a, t) in enumerate(ins):
-        m = re.search(r"BRA (?:`\(\.L_x_\d+\) )?0x([0-9a-f]+)", t)
+        m = re.search(r"BRA(?:\.\w+)*\s+(?:!?U?P\w+,\s*)?(?:`\(\.L_x_\d+\)\s*)?0x([0-9a-f]+)", t)
         if m and "BRA" in t:
             tgt = int(m.group(1), 16)
             if tgt <= a and tgt in addr and i - addr[tgt] >= minlen:
