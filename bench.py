@@ -251,7 +251,10 @@ def run_reference(a):
     kind = res[0][0]
     walls = np.array([w for _, w in res])                  # [procs][outer]
     timed = walls[:, a.warmup:a.warmup + a.steps]          # the K timed full steps
-    sample_step_s = float(timed.max(axis=0).mean())        # all processes done = one sample step
+    # one sample step = the K timed steps of the slowest process / K (all
+    # processes run concurrently; the per-step maximum over processes would
+    # add up stragglers of different steps)
+    sample_step_s = float(timed.sum(axis=1).max()) / a.steps
     users_done = users * procs
     factor = cfg.num_users / users_done
     t_full = sample_step_s * factor                        # whole workload, all host cores
