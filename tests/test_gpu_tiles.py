@@ -100,6 +100,22 @@ def test_production_tile_one_step(monkeypatch, name, users, T, main, split, want
         assert "tail_users" not in v
 
 
+@pytest.mark.parametrize("n,m,main", [(997, 21, "4,256,1"), (601, 17, "4,256,1"), (511, 11, "2,256,1")])
+def test_wide_forward_ragged_one_step(monkeypatch, n, m, main):
+    """The wide-row forward (half the warps, 2R rows each) on ragged shapes:
+    n not a multiple of the tile's rows or of 4 (padding rows in both warp
+    groups' row sets) and m below the tile's compile-time width (padding
+    columns)."""
+    monkeypatch.setenv("NSW_MAIN_TILE", main)
+    monkeypatch.setenv("NSW_SPLIT_USERS", "5")   # 5 users on the forced tile (a lone 6th on the tail tile)
+    rel, expo, cfg = make_instance("cfg2", seed=0, user_slice=(0, 6))
+    rel = np.ascontiguousarray(rel[:, :n])
+    expo = np.ascontiguousarray(expo[:m - 1])
+    v = check_one_step(f"ragged-{n}x{m}", rel, expo, cfg.epsilon, 20)
+    assert (v["R"], v["NT"]) == tuple(int(x) for x in main.split(",")[:2])
+    assert v.get("tail_users", 0) <= 1
+
+
 def test_cfg1_natural_tile_choice_one_step():
     """Full config-1 user count: the automatic choice is the bench's main tile
     on 888 users (6 per SM) plus a 112-user tail on the wide tile."""
