@@ -53,6 +53,10 @@ __host__ __device__ constexpr size_t cl_smem_bytes(int T) {
          48;   // exchange slots [2][CL][P] + two mbarriers (8-byte aligned) + residual scratch
 }
 
+#ifndef NSW_EXP_XTIME
+#define NSW_EXP_XTIME 0   // diagnostics only (see xstamp)
+#endif
+
 // DSMEM push exchange of the per-CTA column totals: every CTA stores its
 // totals into slot [parity][its rank] of every CTA of the cluster with
 // st.async, which completes bytes on the receiver's mbarrier; a receiver
@@ -264,6 +268,17 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   // split in two so independent work can run while the exchange is in
   // flight: post_cols (partials -> barrier -> warp sums -> DSMEM pushes) and
   // collect_cols (wait for every rank's totals -> fin -> barrier)
+  // diagnostics (NSW_EXP_XTIME builds, scripts/cluster_skew.py): thread 0 of
+  // every rank stamps its arrival at / completion of 24 exchanges of the
+  // launch's first user into phase_ns
+  int xcnt = 0;
+  auto xstamp = [&](int which) {
+    if constexpr (NSW_EXP_XTIME) {
+      constexpr int E0 = 100, E = 24;
+      if (tid == 0 && u == a.user0 && a.phase_ns != nullptr && xcnt >= E0 && xcnt < E0 + E)
+        a.phase_ns[size_t(rank) * 2 * E + 2 * (xcnt - E0) + which] = globaltimer_ns();
+    }
+  };
   auto post_cols = [&](S (&v)[MC], bool xon = false, S xval = S(0)) {
     int base = 0, lim = MC;
     rs_rows<S, MC, MC, 16, CG, OpSum>(v, lane, base, lim);
@@ -274,6 +289,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       if (base + j < lim && c < m) red[warp * P + c] = v[j];
     }
     __syncthreads();
+    xstamp(0);
     if constexpr (CL > 1) {
       // thread q sums columns [VE q, VE q + VE) over the warps (warp order,
       // the same bits as a per-column sum) and pushes them as one 16-byte
@@ -336,6 +352,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
       if (xon && tid == m) *xmax = xval;
     }
     __syncthreads();
+    xstamp(1);
+    ++xcnt;
   };
   auto reduce_cols = [&](S (&v)[MC], auto&& fin, bool xon = false, S xval = S(0), S* xmax = nullptr) {
     post_cols(v, xon, xval);

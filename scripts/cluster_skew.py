@@ -1,4 +1,5 @@
-"""Diagnostics (timing-only build NSW_EXP_XTIME=1): per-rank arrival and
+"""Diagnostics (build: python -m paper_2406_10262_b200.build --tag xtime -D NSW_EXP_XTIME=1 --only inst_cl_f32;
+run with NSW_LIB_PATH=paper_2406_10262_b200/libnswrank_b200_xtime.so): per-rank arrival and
 completion stamps of 24 consecutive column exchanges of one config-4 user
 (9-CTA cluster) -- how much of an exchange is the ranks arriving unevenly."""
 import os
