@@ -619,6 +619,13 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     return fail(NSW_ERR_ARG, "bad schedule");
   const int T = config->sinkhorn_max_iters;
   const Variant* var = choose_variant(options->dtype, n, m, T, options->variant);
+  if (const char* e = std::getenv("NSW_TC"); e && std::atoi(e) && var && var->dtype == NSW_F32 && var->CL == 1)
+    for (auto& v : variant_registry())   // experiments: the same tile with the tensor-core adjoint
+      if (v.dtype == 2 && v.M == var->M && v.R == var->R && v.NT == var->NT && v.minb == var->minb &&
+          v.smem(T) <= kMaxSmem) {
+        var = &v;
+        break;
+      }
   if (const char* e = std::getenv("NSW_MAIN_TILE"); e && var && var->CL == 1) {   // experiments: "R,NT[,MINB]"
     int r = 0, nt = 0, mb = 0;
     if (std::sscanf(e, "%d,%d,%d", &r, &nt, &mb) >= 2)

@@ -94,6 +94,7 @@ NSW_REG(8, 256, 1)
 NSW_REG(2, 256, 1)
 NSW_REG(1, 512, 1)
 #elif NSW_M <= 24
+NSW_REG_TC(4, 256, 1)   // config 2 tile with the tensor-core adjoint
 NSW_REG(1, 64, 1)
 NSW_REG(2, 64, 1)
 NSW_REG(4, 64, 4)

@@ -125,19 +125,40 @@ __host__ __device__ constexpr bool stage_inputs() {
   return sizeof(S) == 4 && NT >= 64 && MINB < 7;
 }
 
+// Tensor-core adjoint tile shape: the accumulator's N (the m columns padded to
+// a multiple of 16), TMEM columns allocated (a power of two >= 32) and the
+// K~-tile region, which must also hold the A operand (64 B per row: 8 K slots
+// x hi/lo) that the sweep stages over it.
+template <int M, int R, int NT>
+struct TcShape {
+  static constexpr int kNPC = M <= 16 ? 16 : 32;
+  static constexpr int kNeed = NT * R / 128 * kNPC;
+  static constexpr int kCols = kNeed <= 32 ? 32 : kNeed <= 64 ? 64 : kNeed <= 128 ? 128 : kNeed <= 256 ? 256 : 512;
+};
+template <typename S, int M, int R, int NT, bool TC>
+__host__ __device__ constexpr size_t tile_elems() {
+  constexpr size_t kt = size_t(NT) * R * RowPitch<S, M>::value;
+  constexpr size_t ta = size_t(NT) * R * 64 / sizeof(S);
+  return TC && ta > kt ? ta : kt;
+}
+
 template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __host__ __device__ constexpr size_t step_smem_bytes(int T) {
   constexpr int P = RowPitch<S, M>::value;
   constexpr size_t rows = RowSlots<S, M>::kPad ? 0 : 2 * size_t(NT) * R;
-  return sizeof(S) * (size_t(NT) * R * P + size_t(T + 1) * P + 2 * size_t(NT / 32) * P + 3 * P + rows + 2 * P +
+  return sizeof(S) * (tile_elems<S, M, R, NT, TC>() + size_t(T + 1) * P + 2 * size_t(NT / 32) * P + 3 * P + rows + 2 * P +
                       size_t(NT / 32) + 4 + (stage_inputs<S, NT, MINB>() ? 2 * size_t(NT) * R : 0) + P) +
          32 + 8 * size_t(P) +   // staged inputs (relevance, Imp, exposures in S and float64)
          16 +                   // mbarrier of the cost tile's bulk copy
-         (TC ? size_t(2) * 2 * 512 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
+         (TC ? size_t(2) * 2 * TcShape<M, R, NT>::kNPC * 32 + 64 + 128 : 0);   // tensor-core path: 2 x (hi, lo) B operands + mbarrier
 }
 
 // ---------------------------------------------------------------------------
 // tcgen05 / TMEM helpers (sm_100a) for the tensor-core adjoint accumulation
+#ifndef NSW_TC_EXP
+#define NSW_TC_EXP 0   // diagnostics only: 1 = no A/B staging stores, 2 = no MMAs / waits, 4 = no proxy
+                       // fence, 8 = no waits (wrong results); 16 = one thread issues every block's MMAs
+#endif
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -162,6 +183,15 @@ __device__ __forceinline__ void umma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, u
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %4, {%5, %5, %5, %5}, p;\n\t}\n" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(accum), "r"(kIdescTf32_128x16), "r"(0u));
+}
+// both operands from shared memory (K-major descriptors), D in TMEM
+template <int N>
+__device__ __forceinline__ void umma_tf32_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t accum) {
+  constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | ((128u >> 4) << 24);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(accum), "r"(idesc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar) : "memory");
@@ -224,7 +254,8 @@ template <typename S, int M, int R, int NT, int MINB, bool TC = false>
 __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   // TC: the backward's adjoint G accumulates in tensor memory through tcgen05
   // MMAs (fp32 path, 4-warp CTAs, M <= 16) instead of 2 FFMAs per cell-level.
-  static_assert(!TC || (sizeof(S) == 4 && NT == 128 && M <= 16 && R <= 4), "tensor-core tile shape");
+  static_assert(!TC || (sizeof(S) == 4 && NT % 128 == 0 && M <= 32 && TcShape<M, R, NT>::kNeed <= 512 / MINB),
+                "tensor-core tile shape");
   using F = Fp<S>;
   constexpr int P = RowPitch<S, M>::value;
   constexpr bool PAD = RowSlots<S, M>::kPad;
@@ -256,7 +287,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   nsw_poison_smem(smem_raw);
   const int T = a.T;
   S* Kt = reinterpret_cast<S*>(smem_raw);   // [NT*R][P]  K / K~ / gK rows
-  S* vh = Kt + size_t(NT) * R * P;          // [T+1][P]   v~ history
+  S* vh = Kt + tile_elems<S, M, R, NT, TC>();   // [T+1][P]   v~ history
   S* red = vh + size_t(T + 1) * P;          // [2][NW][P] column partials (double-buffered)
   S* vec0 = red + 2 * NW * P;               // [P] scaling vector / cv
   S* vec1 = vec0 + P;                       // [P] beta / column max
@@ -272,13 +303,14 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
   S* impS = relS + (STAGE ? size_t(NT) * R : 0);   // [NT*R] 1/Imp of the step being differentiated (fp32)
   S* exS = impS + (STAGE ? size_t(NT) * R : 0);   // [P] exposures (0 from column m-1 on)
   double* exD = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(exS + P) + 15) & ~uintptr_t(15));  // [P]
-  // tensor-core path: B operands (2 buffers x hi/lo x 16 rows x 8 tf32) and the MMA mbarrier
+  // tensor-core path: B operands (2 buffers x hi/lo x NPC rows x 8 tf32) and the MMA mbarrier
+  constexpr int NPC = TcShape<M, R, NT>::kNPC;
   uint64_t* bmb = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(exD + P) + 7) & ~uintptr_t(7));
   unsigned char* tc_base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(bmb + 1) + 127) & ~uintptr_t(127));
-  float* Bop = reinterpret_cast<float*>(tc_base);            // [2][2][16 x 8]
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(tc_base + 2048);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_base + 2056);
+  float* Bop = reinterpret_cast<float*>(tc_base);            // [2][2][NPC x 8]
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tc_base + 4 * NPC * 32);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tc_base + 4 * NPC * 32 + 8);
   // slotA: alpha -> u~^T -> u^1 ; slotB: seed g_u (shares slotA's storage
   // when PAD: written after u~^T is in registers, u~^T restored at level T)
   auto slotA = [&](int i) -> S& { return PAD ? Kt[size_t(i) * P + M] : rowA[i]; };
@@ -563,32 +595,101 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 
     // ---------------- seed: W = gx .* X  (sinkhorn.py:272-275) --------------
     if constexpr (TC) {
-      // ---------------- tensor-core adjoint --------------------------------
-      // G (512 x 16, fp32) lives in TMEM as 4 blocks of 128 lanes x 16
-      // columns (row tid + r*128 = block r, lane tid).  Every 4 levels the
-      // rank-8 update G -= [u~ h]_levels [cv v~^{t-1}]'_levels is one
-      // 128x16x8 tf32 MMA per block, split 3xTF32 (hi*hi + hi*lo + lo*hi)
-      // for fp32 accuracy.  A (u~, h pairs) goes registers -> TMEM
-      // (tcgen05.st), B (the column vectors) shared memory; K~ stays in
-      // registers for the whole sweep.
+      // ---------------- tensor-core adjoint (tcgen05 + TMEM) ----------------
+      // The adjoint G (gK = K~ .* G) is only ever accumulated during the sweep
+      // -- the levels read K~, never G -- so its 2T rank-1 terms
+      //   G = a b' - sum_t (u~^t cv^t' + h^t v~^{t-1}')     (sinkhorn.py:288, :297)
+      // are one [rows x 2T] x [2T x m] product: every 4 levels (K = 8) one
+      // 128 x NPC x 8 tf32 MMA per 128-row block accumulates into TMEM, split
+      // 3xTF32 (hi*hi + hi*lo + lo*hi) for fp32 accuracy.  A (u~, h of each
+      // row, two levels per 16-byte store) and B (-cv, -v~^{t-1} per column)
+      // are staged in shared memory in the canonical K-major no-swizzle layout
+      // (8-row x 16-byte core matrices, LBO 128 B between the two K halves,
+      // SBO 256 B between 8-row groups); A lies over the K~ tile, which the
+      // register-resident sweep does not read.  The seed W = K~ .* (a b') is
+      // added in the epilogue.  Row i = tid + r*NT is TMEM lane i % 128 of
+      // block i / 128: the lanes warp (tid / 32) % 4 may access.
+      // The FP32 pipe keeps 3 of the 5 FMAs per cell-level (two row dots and
+      // the column dot); the rank-2 update moves to the tensor pipe.
+      constexpr int NB = NT * R / 128;
+      constexpr int NI = NB < NW ? NB : NW;   // issuing warps (one commit each)
+      constexpr bool PKR_TC = sizeof(S) == 4;  // packed replay dot, as the register-resident sweep
       const int warp_id = tid >> 5;
+      const int lane_id = tid & 31;
       const uint32_t lane_base = uint32_t(32 * (warp_id & 3)) << 16;
+      unsigned char* Abuf = reinterpret_cast<unsigned char*>(Kt);   // [NB][hi, lo][128 rows x 32 B]
       if (warp_id == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "n"(TcShape<M, R, NT>::kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
       }
-      if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(mbar)));
-      for (int q = tid; q < 2 * 2 * 128; q += NT) Bop[q] = 0.f;
+      if (tid == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "n"((NSW_TC_EXP & 16) ? 1 : NI));
+      for (int q = tid; q < 4 * NPC * 8; q += NT) Bop[q] = 0.f;
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t tmem = *tmem_slot;   // column base; D blocks at +16b, A_hi +64+8b, A_lo +96+8b
+      const uint32_t tmem = *tmem_slot;
       const uint32_t mb = smem_u32(mbar);
+      // tf32 split x = hi + lo: hi = x rounded to tf32, lo = x - hi exact in
+      // fp32 (the MMA reads its top 19 bits)
+      auto split = [](float x, float& hi, float& lo) {
+        hi = to_tf32(x);   // round to nearest: |lo| <= 2^-11 |x| (truncation doubles it: 10x worse dC)
+        lo = x - hi;
+      };
+      // A: this thread's rows; row i = tid + r*NT -> block (tid >> 7) + r*NT/128,
+      // row p = tid & 127 of the block; (x0..x3) at K slots 4q..4q+3, hi / lo
+      unsigned char* const a_base = Abuf + size_t(tid >> 7) * 8192 + ((tid & 127) >> 3) * 256 + (tid & 7) * 16;
+      auto put_a = [&](int r, float x0, float x1, float x2, float x3, int q) {
+        if constexpr (NSW_TC_EXP & 1) return;   // timing-only diagnostics build
+        unsigned char* dst = a_base + size_t(r) * (NT / 128) * 8192 + q * 128;
+        float4 hi, lo;
+        split(x0, hi.x, lo.x);
+        split(x1, hi.y, lo.y);
+        split(x2, hi.z, lo.z);
+        split(x3, hi.w, lo.w);
+        *reinterpret_cast<float4*>(dst) = hi;
+        *reinterpret_cast<float4*>(dst + 4096) = lo;
+      };
+      // B: written by the last warp (warp 0 finishes the column reductions):
+      // column n = tid - (NT - 32) < NPC, (x0, x1) at K slots 2j, 2j+1
+      const int bn = tid - (NT - 32);
+      float* const b_base = Bop + (bn >> 3) * 64 + (bn & 7) * 4;
+      auto put_b = [&](int bb, int j, float x0, float x1) {
+        if constexpr (NSW_TC_EXP & 1) return;
+        float* bh = b_base + bb * 2 * NPC * 8 + (j >> 1) * 32 + (j & 1) * 2;
+        float h0, l0, h1, l1;
+        split(x0, h0, l0);
+        split(x1, h1, l1);
+        *reinterpret_cast<float2*>(bh) = make_float2(h0, h1);
+        *reinterpret_cast<float2*>(bh + NPC * 8) = make_float2(l0, l1);
+      };
+      int chunk = 0;   // chunks issued so far; B buffer of the current chunk = chunk & 1
+      auto issue = [&]() {
+        if (!(NSW_TC_EXP & 2) && lane_id == 0 && ((NSW_TC_EXP & 16) ? warp_id == NW - 1 : warp_id < NI)) {
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const float* bb = Bop + (chunk & 1) * 2 * NPC * 8;
+          const uint64_t bh = umma_desc_kmajor(smem_u32(bb), 128, 256);
+          const uint64_t bl = umma_desc_kmajor(smem_u32(bb + NPC * 8), 128, 256);
+#pragma unroll
+          for (int b = (NSW_TC_EXP & 16) ? 0 : warp_id; b < NB; b += (NSW_TC_EXP & 16) ? 1 : NI) {
+            const uint32_t d = tmem + uint32_t(b * NPC);
+            const uint64_t ah = umma_desc_kmajor(smem_u32(Abuf + size_t(2 * b) * 4096), 128, 256);
+            const uint64_t al = umma_desc_kmajor(smem_u32(Abuf + size_t(2 * b + 1) * 4096), 128, 256);
+            umma_tf32_ss<NPC>(d, ah, bh, chunk > 0 ? 1u : 0u);
+            umma_tf32_ss<NPC>(d, ah, bl, 1u);
+            umma_tf32_ss<NPC>(d, al, bh, 1u);
+          }
+          umma_commit(mb);
+        }
+        __syncwarp();
+        ++chunk;
+      };
 
       S Kr[R][M];
       S ut[R];
-      float av[R][8];
+      S gs[R];   // seed g_u (row sums of W), live only until the first level
+      S ai[R];   // seed row factor a_i = u~^T_i r_i / Imp_i
       {
         S c[M], ex[M];
         load_ex(ex);
@@ -600,148 +701,140 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
           lds_vec<S, M>(Kr[r], Kt + size_t(i) * P);
           ut[r] = slotA(i);
           const S rr = rel_of(i);
+          ai[r] = mul_(mul_(rr, impv_of(i)), ut[r]);
           S gsum = S(0);
 #pragma unroll
           for (int k = 0; k < M; ++k) {
-            if (k < m - 1) {
-              const S W = mul_(gx_of(rr, ex[k], impv_of(i)), mul_(mul_(Kr[r][k], ut[r]), vT[k]));
-              gsum += W;
-              c[k] += W;
-            }
+            const S W = mul_(Kr[r][k], mul_(ai[r], mul_(ex[k], vT[k])));
+            gsum += W;
+            c[k] += W;
           }
-          slotB(i) = gsum;
-#pragma unroll
-          for (int q = 0; q < 8; ++q) av[r][q] = 0.f;
+          gs[r] = gsum;
         }
         cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
-          vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));
+          vec0[k] = mul_(mul_(vh[size_t(Th) * P + k], tot), inv_mass(k));   // cv^T = v~^T g_v / colmass
         });
       }
-      int chunk = 0, buf = 0;
-      for (int t = Th; t >= 1; --t) {
-        const int j = (Th - t) & 3;       // slot of this level in the current chunk
-        S cv[M], vpp[M], c[M];
+      mark(5);
+      S up[R], hp[R];   // (u~, h) of the even level of the current pair
+      S live[R];        // 1 on real rows, 0 on padding rows (finite MMA inputs)
+#pragma unroll
+      for (int r = 0; r < R; ++r) live[r] = ok(r) ? S(1) : S(0);
+      // ODD: the level's K slot pair j = (Th - t) & 3 is odd (it completes a
+      // 16-byte A store); the first level (t = Th) has j = 0
+      auto level_tc = [&](const int t, auto first_c, auto last_c, auto odd_c) {
+        constexpr bool FIRST = decltype(first_c)::value;
+        constexpr bool LAST = decltype(last_c)::value;
+        constexpr bool ODD = decltype(odd_c)::value;
+        const int j = (Th - t) & 3;
+        S cv[M], c[M];
         lds_vec<S, M>(cv, vec0);
-        lds_vec<S, M>(vpp, vh + size_t(t >= 2 ? t - 2 : 0) * P);
-        if (tid < 16) {                   // B rows: -cv^t and -v~^{t-1} of column tid
-          const float x0 = tid < m ? -vec0[tid] : 0.f;
-          const float x1 = tid < m ? -vh[size_t(t - 1) * P + tid] : 0.f;
-          float* bh = Bop + (buf * 2 + 0) * 128;
-          float* bl = Bop + (buf * 2 + 1) * 128;
-          const int o0 = (tid & 7) * 4 + (tid >> 3) * 64 + (j >> 1) * 32 + (j & 1) * 2;
-          const float h0 = to_tf32(x0), h1 = to_tf32(x1);
-          bh[o0] = h0;
-          bh[o0 + 1] = h1;
-          bl[o0] = to_tf32(x0 - h0);
-          bl[o0 + 1] = to_tf32(x1 - h1);
+        const S* vpp1 = vh + size_t(t - 1) * P;
+        const S* vppp = vh + size_t(LAST ? 0 : t - 2) * P;
+        if (bn >= 0 && bn < NPC) {
+          const float x0 = bn < m ? -vec0[bn] : 0.f;
+          const float x1 = bn < m ? -vpp1[bn] : 0.f;
+          put_b(chunk & 1, j, x0, x1);
+          if constexpr (LAST)
+            for (int jj = j + 1; jj < 4; ++jj) put_b(chunk & 1, jj, 0.f, 0.f);   // short final chunk
         }
-        const bool first = t == Th;
-        const bool replay = t >= 2;
 #pragma unroll
         for (int k = 0; k < M; ++k) c[k] = S(0);
+        S uc[R], hc[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int i = tid + r * NT;
-          const S sig = rdot<S, M, CH, PK>(Kr[r], cv);
-          const S den = rdot<S, M, CH, PKD>(Kr[r], vpp);
-          S gs = S(0);
-          if (first) {
-            gs = slotB(i);
-            slotA(i) = ut[r];
+          const S sig = rdot<S, M, CH, true>(Kr[r], cv);
+          S den = S(1);
+          if constexpr (!LAST) {
+            S vpp[M];
+            lds_vec<S, M>(vpp, vppp);
+            den = rdot<S, M, CH, PKR_TC>(Kr[r], vpp);
           }
-          const S h = ut[r] * (gs - ut[r] * sig);
-#pragma unroll
-          for (int k = 0; k < M; ++k) c[k] = fma(Kr[r][k], h, c[k]);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (q == j) {
-              av[r][2 * q] = ut[r];
-              av[r][2 * q + 1] = h;
-            }
-          }
-          ut[r] = masked_rcp(den, ok(r) && replay);
+          const S h = ut[r] * (FIRST ? gs[r] - ut[r] * sig : -(ut[r] * sig));
+          uc[r] = ut[r] * live[r];
+          hc[r] = h;
+          if constexpr (!LAST) axpy_<S, M, true>(c, Kr[r], h);
+          if constexpr (!LAST) ut[r] = rcp_clamped(den);
         }
-        if (t >= 2) {
+        if constexpr (ODD || LAST) {
+          // the chunk's first A store waits for the previous chunk's MMAs
+          if (!(NSW_TC_EXP & 10) && (j == 1 || (LAST && j == 0)) && chunk > 0) mbar_wait(mb, uint32_t((chunk - 1) & 1));
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if constexpr (ODD) put_a(r, up[r], hp[r], uc[r], hc[r], j >> 1);
+            else put_a(r, uc[r], hc[r], 0.f, 0.f, j >> 1);
+          }
+          // generic-proxy stores -> the MMA (async proxy), before the barrier
+          // that precedes the issue
+          if (!(NSW_TC_EXP & 4) && (j == 3 || LAST)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        } else {
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            up[r] = uc[r];
+            hp[r] = hc[r];
+          }
+        }
+        if constexpr (!LAST) {
           cta_reduce_cols<S, M, NT, OpSum>(c, red, m, [&](int k, S tot) {
             const S vpk = vh[size_t(t - 1) * P + k];
             const S gv = -mul_(vpk, tot);
             vec0[k] = mul_(mul_(vpk, gv), inv_mass(k));
           });
-        }
-        if (j == 3 || t == 1) {
-          // flush the chunk: A -> TMEM, then one elected thread issues the MMAs
-          if (chunk > 0) mbar_wait(mb, uint32_t((chunk - 1) & 1));
-          asm volatile("tcgen05.fence::after_thread_sync;");
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            float hi[8], lo[8];
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              hi[q] = to_tf32(av[r][q]);
-              lo[q] = to_tf32(av[r][q] - hi[q]);
-              av[r][q] = 0.f;
-            }
-            tmem_st8(tmem + lane_base + uint32_t(64 + 8 * r), hi);
-            tmem_st8(tmem + lane_base + uint32_t(96 + 8 * r), lo);
-          }
-          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile("tcgen05.fence::before_thread_sync;");
+        } else {
           __syncthreads();
-          if (tid == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint64_t bh = umma_desc_kmajor(smem_u32(Bop + (buf * 2 + 0) * 128), 128, 256);
-            const uint64_t bl = umma_desc_kmajor(smem_u32(Bop + (buf * 2 + 1) * 128), 128, 256);
-#pragma unroll
-            for (int b = 0; b < R; ++b) {
-              const uint32_t d = tmem + uint32_t(16 * b);
-              const uint32_t ah = tmem + uint32_t(64 + 8 * b), al = tmem + uint32_t(96 + 8 * b);
-              umma_tf32_ts(d, ah, bh, chunk > 0 ? 1u : 0u);
-              umma_tf32_ts(d, ah, bl, 1u);
-              umma_tf32_ts(d, al, bh, 1u);
-            }
-            umma_commit(mb);
-          }
-          ++chunk;
-          buf ^= 1;
-          if (tid < 16) {   // the next chunk's B buffer starts from zero (short final chunk)
-            float* bh = Bop + (buf * 2 + 0) * 128;
-            float* bl = Bop + (buf * 2 + 1) * 128;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int o = (tid & 7) * 4 + (tid >> 3) * 64 + (q >> 1) * 32 + (q & 1) * 2;
-              bh[o] = bh[o + 1] = 0.f;
-              bl[o] = bl[o + 1] = 0.f;
-            }
-          }
+        }
+        if (LAST || (ODD && j == 3)) issue();
+      };
+      using TT = std::true_type;
+      using FF = std::false_type;
+      if (Th == 1) {
+        level_tc(1, TT{}, TT{}, FF{});
+      } else {
+        level_tc(Th, TT{}, FF{}, FF{});
+        int t = Th - 1;   // always an odd-slot level here
+        for (; t >= 3; t -= 2) {
+          level_tc(t, FF{}, FF{}, TT{});
+          level_tc(t - 1, FF{}, FF{}, FF{});
+        }
+        if (t == 2) {
+          level_tc(2, FF{}, FF{}, TT{});
+          level_tc(1, FF{}, TT{}, FF{});
+        } else {
+          level_tc(1, FF{}, TT{}, TT{});
         }
       }
-      mbar_wait(mb, uint32_t((chunk - 1) & 1));
+      mark(6);
+      if constexpr (!(NSW_TC_EXP & 2)) mbar_wait(mb, uint32_t((chunk - 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
-      // gK = W + K~ .* G, G read back from TMEM
-      S ex[M];
-      load_ex(ex);
+      // gK = K~ .* (a b' + G), G read back from TMEM, over the tile
+      {
+        S ex[M], vTe[M];
+        load_ex(ex);
+        lds_vec<S, M>(vTe, vh + size_t(Th) * P);
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = tid + r * NT;
-        float g16[16];
-        tmem_ld16(tmem + lane_base + uint32_t(16 * r), g16);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        S gk[M];
-        const S uT = slotA(i);
-        const S rr = rel_of(i);
+        for (int r = 0; r < R; ++r) {
+          const int i = tid + r * NT;
+          const int b = i >> 7;
+          float g[NPC];
 #pragma unroll
-        for (int k = 0; k < M; ++k) {
-          const S W = (k < m - 1) ? mul_(gx_of(rr, ex[k], impv_of(i)), mul_(mul_(Kr[r][k], uT), vT[k])) : S(0);
-          gk[k] = fma(Kr[r][k], S(g16[k]), W);
+          for (int q = 0; q < NPC / 16; ++q) {
+            float g16[16];
+            tmem_ld16(tmem + lane_base + uint32_t(b * NPC + 16 * q), g16);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) g[16 * q + e] = g16[e];
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          S gk[M];
+#pragma unroll
+          for (int k = 0; k < M; ++k) gk[k] = ok(r) ? mul_(Kr[r][k], fma(ai[r], mul_(ex[k], vTe[k]), S(g[k]))) : S(0);
+          sts_vec<S, M>(Kt + size_t(i) * P, gk);
         }
-        sts_vec<S, M>(Kt + size_t(i) * P, gk);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncthreads();
       if (warp_id == 0) {
         asm volatile("tcgen05.fence::after_thread_sync;");
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TcShape<M, R, NT>::kCols));
       }
     } else {
     S A[R][M];  // adjoint G: gK = W + K~ .* G
@@ -1091,7 +1184,7 @@ forward_iterations:
 #ifndef NSW_WIDE_FWD
 #define NSW_WIDE_FWD 1
 #endif
-  if constexpr (NSW_WIDE_FWD && sizeof(S) == 4 && MINB == 1 && NT >= 256 && R <= 4 && M <= 32 && !TC &&
+  if constexpr (NSW_WIDE_FWD && sizeof(S) == 4 && MINB == 1 && NT >= 256 && R <= 4 && M <= 32 &&
                 2 * R * M + 2 * M + 2 * R + 24 <= (65536 / NT < 255 ? 65536 / NT : 255)) {
     if (!tolm) {
       constexpr int NTA = NT / 2, RA = 2 * R;

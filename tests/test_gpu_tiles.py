@@ -130,3 +130,30 @@ def test_cfg4_cluster_tile_one_step():
     rel, expo, cfg = make_instance("cfg4", seed=0, user_slice=(0, 2))
     v = check_one_step("cfg4", rel, expo, cfg.epsilon, 30)
     assert v["M"] >= 51
+
+
+@pytest.mark.parametrize("T", [30, 31, 29, 32])
+def test_tensor_core_adjoint_cfg2_tile_one_step(monkeypatch, T):
+    """The config-2 tile with the tensor-core adjoint (tcgen05 MMAs into TMEM,
+    NSW_TC=1) and its concurrent tail; T = 29..32 ends the reverse sweep on
+    every slot of the 4-level MMA chunk (short final chunks)."""
+    monkeypatch.setenv("NSW_TC", "1")
+    monkeypatch.setenv("NSW_MAIN_TILE", "4,256,1")
+    monkeypatch.setenv("NSW_SPLIT_USERS", "3")
+    rel, expo, cfg = make_instance("cfg2", seed=0, user_slice=(0, 6))
+    v = check_one_step(f"cfg2-tc-T{T}", rel, expo, cfg.epsilon, T)
+    assert (v["M"], v["R"], v["NT"]) == (21, 4, 256)
+    assert v.get("tail_users") == 3
+
+
+def test_tensor_core_adjoint_ragged_one_step(monkeypatch):
+    """Tensor-core adjoint on a ragged shape: padding rows in the last
+    128-row MMA block and padding columns in the accumulator."""
+    monkeypatch.setenv("NSW_TC", "1")
+    monkeypatch.setenv("NSW_MAIN_TILE", "4,256,1")
+    monkeypatch.setenv("NSW_SPLIT_USERS", "5")
+    rel, expo, cfg = make_instance("cfg2", seed=0, user_slice=(0, 6))
+    rel = np.ascontiguousarray(rel[:, :997])
+    expo = np.ascontiguousarray(expo[:16])
+    v = check_one_step("ragged-tc-997x17", rel, expo, cfg.epsilon, 21)
+    assert (v["R"], v["NT"]) == (4, 256)
