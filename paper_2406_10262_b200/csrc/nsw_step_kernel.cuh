@@ -273,8 +273,8 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel(const StepArgs<S> a) {
 #define NSW_PK_DOT 0
 #endif
 #ifndef NSW_PK_FWD_AXPY
-#define NSW_PK_FWD_AXPY 0
-#endif
+#define NSW_PK_FWD_AXPY 1   // the forward's column axpy packed (broadcast u~): config 3 +1.5 %, configs 1-2 neutral
+#endif                      // (profiles/r02/ab_pk_fwd_axpy.txt); FFMA2 rounds like two FFMAs: same bits
   constexpr bool PKD = PK || (NSW_PK_DOT && sizeof(S) == 4);
   constexpr bool PKF = PK || (NSW_PK_FWD_AXPY && sizeof(S) == 4);
   // register-lean backward (tiles packed 7 per SM): the v~ history rows are
