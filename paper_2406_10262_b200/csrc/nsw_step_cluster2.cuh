@@ -177,8 +177,7 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl2(const StepArgs<S> a) {
     __syncthreads();
   };
 
-  // exposure and v~^T segments are re-read where the seed and the gK pass
-  // need them: nothing but G, KX and the row scalings lives across the loop
+  // exposure and v~^T segments are re-read where the seed and the gK pass need them
   auto load_ex = [&](S (&ex)[MC]) {
 #pragma unroll
     for (int j = 0; j < MC; ++j) ex[j] = (col(j) < m - 1) ? a.expo[min(col(j), m - 2)] : S(0);
@@ -187,50 +186,38 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl2(const StepArgs<S> a) {
   const int step = a.state[ST_STEP];
   const S ibc1 = S(1.0 / a.bc[2 * step]), ibc2 = S(1.0 / a.bc[2 * step + 1]);
 
-  S G[R][MC];    // Y: adjoint of K~
-  S utY[R], utX[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    utY[r] = S(0);
-    utX[r] = S(0);
-#pragma unroll
-    for (int j = 0; j < MC; ++j) G[r][j] = S(0);
-  }
+  for (int k0 = 0; k0 < nu; k0 += 2) {
+    const bool hasB = k0 + 1 < nu;
 
-  for (int s = 0; s <= nu; ++s) {
-    const bool hasY = s < nu, hasX = s >= 1;
-    const int sy = s & 1, sx = sy ^ 1;
-    S* const KtY = Ktof(sy);
-    S* const KtX = Ktof(sx);
-    S* const sbY = slof(sy);
-    S* const sbX = slof(sx);
-    const int uY = hasY ? user(s) : 0, uX = hasX ? user(s - 1) : 0;
-    S* const huY = a.hist + size_t(uY) * (T + 1) * m;
-    S* const huX = a.hist + size_t(uX) * (T + 1) * m;
-    const S* const reluY = a.rel + size_t(uY) * n + r0;
-    S* const vrY = sbY + L::O_VR;
-    S* const vTrY = sbY + L::O_VTR;
-    S* const vec0Y = sbY + L::O_VEC0;
-    S* const vec0X = sbX + L::O_VEC0;
-    S* const rowAY = sbY + L::O_ROWA;
-    S* const rowBY = sbY + L::O_ROWB;
-    auto vrow = [&](int t) -> S* { return vrY + (t & 3) * P; };
-    auto load_row = [&](S* dst, int t) {
-      for (int k = tid; k < P; k += NT) cp_async_zfill(dst + k, huY + size_t(t) * m + (k < m ? k : 0), k < m);
-      cp_async_commit();
-    };
-    auto foreach_cell = [&](auto&& f) {
-      if (vec_ok) {
-        for (int q = tid; q < ncell / V; q += NT) f(q * V, q);
-      } else {
-        for (int e = tid; e < ncell; e += NT) f(e, -1);
-      }
-    };
-
-    if (hasY) {
-      // ---- Y: rebuild the previous step's K~, u~^T, policy, seed ----
-      S* const Cu = a.C + ubase(uY);
+    // ================= backward + Adam, one user after the other =================
+    for (int w = 0; w < (hasB ? 2 : 1); ++w) {
+      const int si = w;
+      const int uY = user(k0 + w);
+      S* const KtY = Ktof(si);
+      S* const sbY = slof(si);
+      S* const huY = a.hist + size_t(uY) * (T + 1) * m;
+      const S* const reluY = a.rel + size_t(uY) * n + r0;
+      S* const vrY = sbY + L::O_VR;
+      S* const vTrY = sbY + L::O_VTR;
+      S* const vec0Y = sbY + L::O_VEC0;
       S* const vec1 = sbY + L::O_VEC1;
+      S* const vec2 = sbY + L::O_VEC2;
+      S* const rowAY = sbY + L::O_ROWA;
+      S* const rowBY = sbY + L::O_ROWB;
+      S* const Cu = a.C + ubase(uY);
+      auto vrow = [&](int t) -> S* { return vrY + (t & 3) * P; };
+      auto load_row = [&](S* dst, int t) {
+        for (int k = tid; k < P; k += NT) cp_async_zfill(dst + k, huY + size_t(t) * m + (k < m ? k : 0), k < m);
+        cp_async_commit();
+      };
+      auto foreach_cell = [&](auto&& f) {
+        if (vec_ok) {
+          for (int q = tid; q < ncell / V; q += NT) f(q * V, q);
+        } else {
+          for (int e = tid; e < ncell; e += NT) f(e, -1);
+        }
+      };
+      // ---- rebuild the previous step's K~, u~^T, policy, seed ----
       if (tid < m) vec1[tid] = a.beta[size_t(uY) * m + tid];
       for (int i = tid; i < nloc; i += NT) rowAY[i] = a.alpha[size_t(uY) * n + r0 + i];
       load_row(vTrY, T);
@@ -283,110 +270,48 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl2(const StepArgs<S> a) {
           }
         });
       }
-      // seed W = gx .* X
-      S c[MC], ex[MC], vT[MC];
-      load_ex(ex);
-#pragma unroll
-      for (int j = 0; j < MC; ++j) {
-        c[j] = S(0);
-        vT[j] = vTrY[col(j)];
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int il = lrow(r);
-        S kr[MC];
-        ld_seg<Tl, S, MC>(kr, KtY, il, g);
-        utY[r] = rowAY[il];
-        const S rr = ok(r) ? reluY[il] : S(0);
-        const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
-        const S inv_imp = S(1.0 / double(imp_i));
-        S gsum = S(0);
+      S G[R][MC];    // adjoint of K~
+      S Kr[R][MC];   // K~ row segments, register-resident for the whole sweep
+      S ut[R];
+      {
+        // seed W = gx .* X
+        S c[MC], ex[MC], vT[MC];
+        load_ex(ex);
 #pragma unroll
         for (int j = 0; j < MC; ++j) {
-          G[r][j] = S(0);
-          if (col(j) < m - 1) {
-            const S W = mul_(gx_of(rr, ex[j], inv_imp), mul_(mul_(kr[j], utY[r]), vT[j]));
-            gsum += W;
-            c[j] += W;
-          }
+          c[j] = S(0);
+          vT[j] = vTrY[col(j)];
         }
-        gsum = group_sum<S, CG>(gsum);
-        if (g == 0) rowBY[il] = gsum;
-      }
-      reduce_cols(c, sy, sbY, [&](int k, S tot) { vec0Y[k] = mul_(mul_(vTrY[k], tot), inv_mass(k)); });
-    }
-
-    if (hasX) {
-      // ---- X: absorb beta = lvi, alpha = -rowmax(K + beta) (K = -C/eps left
-      // in the tile by X's Adam pass one stage ago) ----
-      const S* const vec2 = sbX + L::O_VEC2;
-      if (rank == 0 && tid < m) {
-        a.beta[size_t(uX) * m + tid] = vec2[tid];
-        huX[tid] = S(1);
-      }
-      if (tid < m) vec0X[tid] = S(1);
-      S bt[MC];
-#pragma unroll
-      for (int j = 0; j < MC; ++j) bt[j] = vec2[col(j)];
-#pragma unroll 1
-      for (int r = 0; r < R; ++r) {
-        const int il = lrow(r);
-        S kr[MC];
-        ld_seg<Tl, S, MC>(kr, KtX, il, g);
-        S mx = F::ninf();
-#pragma unroll
-        for (int j = 0; j < MC; ++j)
-          if (col(j) < m) mx = fmax(mx, add_(kr[j], bt[j]));
-        mx = group_max<S, CG>(mx);
-        const S al = -mx;
-        if (g == 0 && ok(r)) a.alpha[size_t(uX) * n + r0 + il] = al;
-#pragma unroll
-        for (int j = 0; j < MC; ++j)
-          kr[j] = (ok(r) && col(j) < m) ? F::exp_fast(add_(add_(kr[j], bt[j]), al)) : S(0);
-        st_seg<Tl, S, MC>(KtX, il, g, kr);   // own rows only: no barrier needed before the loop's loads
-      }
-#pragma unroll
-      for (int r = 0; r < R; ++r) utX[r] = S(0);
-    }
-    __syncthreads();
-
-    // ---- the paired loop: forward iteration t of X, reverse level T+1-t of Y ----
-    for (int t = 1; t <= T; ++t) {
-      const int tb = T + 1 - t;
-      if (hasX) {
-        S vv[MC], c[MC];
-        S KX[R][MC];   // X's K~ row segments: re-read every iteration (the registers are the level's working set)
-#pragma unroll
-        for (int r = 0; r < R; ++r) ld_seg<Tl, S, MC>(KX[r], KtX, lrow(r), g);
-#pragma unroll
-        for (int j = 0; j < MC; ++j) vv[j] = vec0X[col(j)];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const S rp = F::rcp_fast(rdot_g<S, MC, CG>(KX[r], vv));
-          utX[r] = ok(r) ? rp : S(0);
+          const int il = lrow(r);
+          ld_seg<Tl, S, MC>(Kr[r], KtY, il, g);
+          ut[r] = rowAY[il];
+          const S rr = ok(r) ? reluY[il] : S(0);
+          const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
+          const S inv_imp = S(1.0 / double(imp_i));
+          S gsum = S(0);
+#pragma unroll
+          for (int j = 0; j < MC; ++j) {
+            G[r][j] = S(0);
+            if (col(j) < m - 1) {
+              const S W = mul_(gx_of(rr, ex[j], inv_imp), mul_(mul_(Kr[r][j], ut[r]), vT[j]));
+              gsum += W;
+              c[j] += W;
+            }
+          }
+          gsum = group_sum<S, CG>(gsum);
+          if (g == 0) rowBY[il] = gsum;
         }
-#pragma unroll
-        for (int j = 0; j < MC; ++j) c[j] = S(0);
-#pragma unroll
-        for (int r = 0; r < R; ++r) axpy_<S, MC, true>(c, KX[r], utX[r]);
-        stage_cols(c, sbX);
+        reduce_cols(c, si, sbY, [&](int k, S tot) { vec0Y[k] = mul_(mul_(vTrY[k], tot), inv_mass(k)); });
       }
-      if (hasY && t > 1) {   // totals of level tb + 1, pushed one phase ago
-        const S* rp1 = vrow(tb);
-        collect_cols(sy, sbY, [&](int k, S tot) {
-          const S vpk = rp1[k];
-          vec0Y[k] = mul_(mul_(vpk, -mul_(vpk, tot)), inv_mass(k));
-        });
-      }
-      __syncthreads();   // A: X's partials and Y's column vector are published
-      if (hasX) push_cols(sx, sbX);
-      if (hasY) {
-        // stream row tb-3 into the slot row tb+1 held (last read at level tb+2)
-        if (tb >= 3) load_row(vrow(tb - 3), tb - 3);
+      // ---- reverse sweep (as step_kernel_cl: the exchange is exposed here) ----
+      for (int t = T; t >= 1; --t) {
+        if (t >= 3) load_row(vrow(t - 3), t - 3);
         S cv[MC], vp[MC], vpp[MC], c[MC];
-        const S* rp = vrow(tb - 1);
-        const S* rpp = vrow(tb >= 2 ? tb - 2 : 0);
-        const bool first = tb == T;
+        const S* rp = vrow(t - 1);
+        const S* rpp = vrow(t >= 2 ? t - 2 : 0);
+        const bool first = t == T;
 #pragma unroll
         for (int j = 0; j < MC; ++j) {
           cv[j] = vec0Y[col(j)];
@@ -397,82 +322,47 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl2(const StepArgs<S> a) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const int il = lrow(r);
-          S kr[MC];
-          ld_seg<Tl, S, MC>(kr, KtY, il, g);
-          const S sig = rdot_g<S, MC, CG>(kr, cv);
-          const S den = rdot_g<S, MC, CG>(kr, vpp);
+          const S sig = rdot_g<S, MC, CG>(Kr[r], cv);
+          const S den = rdot_g<S, MC, CG>(Kr[r], vpp);
           const S gs = first ? rowBY[il] : S(0);
-          const S h = utY[r] * (gs - utY[r] * sig);
-          axpy_<S, MC, true>(G[r], cv, -utY[r]);
+          const S h = ut[r] * (gs - ut[r] * sig);
+          axpy_<S, MC, true>(G[r], cv, -ut[r]);
           axpy_<S, MC, true>(G[r], vp, -h);
-          axpy_<S, MC, true>(c, kr, h);
-          utY[r] = (ok(r) && tb >= 2) ? F::rcp_fast(den) : S(0);
+          axpy_<S, MC, true>(c, Kr[r], h);
+          ut[r] = (ok(r) && t >= 2) ? F::rcp_fast(den) : S(0);
         }
-        if (tb >= 2) {
-          cp_async_wait_all();   // row tb-3 lands before barrier B publishes it
-          stage_cols(c, sbY);
+        if (t >= 2) {
+          cp_async_wait_all();   // row t-3 lands before the reduction's barrier publishes it
+          reduce_cols(c, si, sbY, [&](int k, S tot) {
+            const S vpk = rp[k];
+            vec0Y[k] = mul_(mul_(vpk, -mul_(vpk, tot)), inv_mass(k));
+          });
         }
       }
-      if (hasX) {
-        collect_cols(sx, sbX, [&](int k, S tot) {
-          const S vn = F::div_fast(mass(k), tot);
-          vec0X[k] = vn;
-          if (rank == 0) huX[size_t(t) * m + k] = vn;
-        });
-      }
-      __syncthreads();   // B: Y's partials and X's v~ are published
-      if (hasY && tb >= 2) push_cols(sy, sbY);
-    }
-
-    if (hasX) {
-      // ---- X: per-item impact terms, float64, completed across the group ----
-      S vv[MC];
+      // ---- gK = W + K~ .* G over the tile, then the Adam ascent ----
+      {
+        S ex[MC], vT[MC];
+        load_ex(ex);
 #pragma unroll
-      for (int j = 0; j < MC; ++j) vv[j] = vec0X[col(j)];
-      const S* const reluX = a.rel + size_t(uX) * n + r0;
+        for (int j = 0; j < MC; ++j) vT[j] = vTrY[col(j)];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int il = lrow(r);
-        const double rr = ok(r) ? double(reluX[il]) : 0.0;
-        S kr[MC];
-        ld_seg<Tl, S, MC>(kr, KtX, il, g);
-        double acc = 0.0;
+        for (int r = 0; r < R; ++r) {
+          const int il = lrow(r);
+          S gk[MC];
+          const S uT = rowAY[il];
+          const S rr = ok(r) ? reluY[il] : S(0);
+          const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
+          const S inv_imp = S(1.0 / double(imp_i));
 #pragma unroll
-        for (int j = 0; j < MC; ++j)
-          if (col(j) < m - 1)
-            acc = fma(rr * a.expo_d[min(col(j), m - 2)], double(mul_(mul_(kr[j], utX[r]), vv[j])), acc);
-        acc = group_sum<double, CG>(acc);
-        if (g == 0 && ok(r)) a.partial[size_t(uX) * n + r0 + il] = acc;
-      }
-    }
-
-    if (hasY) {
-      // ---- Y: gK = W + K~ .* G over the tile, then the Adam ascent ----
-      S ex[MC], vT[MC];
-      load_ex(ex);
-#pragma unroll
-      for (int j = 0; j < MC; ++j) vT[j] = vTrY[col(j)];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int il = lrow(r);
-        S kr[MC], gk[MC];
-        ld_seg<Tl, S, MC>(kr, KtY, il, g);
-        const S uT = rowAY[il];
-        const S rr = ok(r) ? reluY[il] : S(0);
-        const S imp_i = ok(r) ? S(a.imp[r0 + il]) : S(1);
-        const S inv_imp = S(1.0 / double(imp_i));
-#pragma unroll
-        for (int j = 0; j < MC; ++j) {
-          const S W = (col(j) < m - 1) ? mul_(gx_of(rr, ex[j], inv_imp), mul_(mul_(kr[j], uT), vT[j])) : S(0);
-          gk[j] = fma(kr[j], G[r][j], W);
+          for (int j = 0; j < MC; ++j) {
+            const S W = (col(j) < m - 1) ? mul_(gx_of(rr, ex[j], inv_imp), mul_(mul_(Kr[r][j], uT), vT[j])) : S(0);
+            gk[j] = fma(Kr[r][j], G[r][j], W);
+          }
+          st_seg<Tl, S, MC>(KtY, il, g, gk);
         }
-        st_seg<Tl, S, MC>(KtY, il, g, gk);
       }
-      S* const vec1 = sbY + L::O_VEC1;
-      S* const vec2 = sbY + L::O_VEC2;
       if (tid < m) vec2[tid] = a.warm_start ? add_(vec1[tid], F::log_(vTrY[tid])) : S(0);
       __syncthreads();
-      S* const Cu = a.C + ubase(uY);
       S* const mu = a.am + ubase(uY);
       S* const vu = a.av + ubase(uY);
       auto adam = [&](S& cc, S& mm, S& vv, S gk) {
@@ -510,8 +400,120 @@ __global__ void __launch_bounds__(NT, 1) step_kernel_cl2(const StepArgs<S> a) {
           vu[e0] = vv;
         }
       });
+      __syncthreads();   // the tile now holds K = -C/eps of this user's forward
     }
-    __syncthreads();   // Y's tile (K of its forward) and vec2 are complete before the next stage reads them
+
+    // ================= the two forwards, interleaved =================
+    const int uA = user(k0), uB = hasB ? user(k0 + 1) : uA;
+    S* const sbA = slof(0);
+    S* const sbB = slof(1);
+    S* const vec0A = sbA + L::O_VEC0;
+    S* const vec0B = sbB + L::O_VEC0;
+    S* const huA = a.hist + size_t(uA) * (T + 1) * m;
+    S* const huB = a.hist + size_t(uB) * (T + 1) * m;
+    S KA[R][MC], KB[R][MC];   // K~ row segments of the two users
+    S utA[R], utB[R];
+    // absorb beta = lvi, alpha = -rowmax(K + beta)
+    auto absorb = [&](S (&K)[R][MC], S (&ut)[R], int u, const S* Kt, S* sb, S* hu) {
+      const S* const vec2 = sb + L::O_VEC2;
+      if (rank == 0 && tid < m) {
+        a.beta[size_t(u) * m + tid] = vec2[tid];
+        hu[tid] = S(1);
+      }
+      if (tid < m) sb[L::O_VEC0 + tid] = S(1);
+      S bt[MC];
+#pragma unroll
+      for (int j = 0; j < MC; ++j) bt[j] = vec2[col(j)];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int il = lrow(r);
+        ld_seg<Tl, S, MC>(K[r], Kt, il, g);
+        S mx = F::ninf();
+#pragma unroll
+        for (int j = 0; j < MC; ++j)
+          if (col(j) < m) mx = fmax(mx, add_(K[r][j], bt[j]));
+        mx = group_max<S, CG>(mx);
+        const S al = -mx;
+        if (g == 0 && ok(r)) a.alpha[size_t(u) * n + r0 + il] = al;
+#pragma unroll
+        for (int j = 0; j < MC; ++j)
+          K[r][j] = (ok(r) && col(j) < m) ? F::exp_fast(add_(add_(K[r][j], bt[j]), al)) : S(0);
+        ut[r] = S(0);
+      }
+    };
+    absorb(KA, utA, uA, Ktof(0), sbA, huA);
+    if (hasB) {
+      absorb(KB, utB, uB, Ktof(1), sbB, huB);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        utB[r] = S(0);
+#pragma unroll
+        for (int j = 0; j < MC; ++j) KB[r][j] = S(0);
+      }
+    }
+    __syncthreads();
+    // one forward iteration's compute: row dots, u~, column partials -> red
+    auto fwd_compute = [&](const S (&K)[R][MC], S (&ut)[R], S* sb) {
+      S vv[MC], c[MC];
+      const S* vec0 = sb + L::O_VEC0;
+#pragma unroll
+      for (int j = 0; j < MC; ++j) vv[j] = vec0[col(j)];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const S rp = F::rcp_fast(rdot_g<S, MC, CG>(K[r], vv));
+        ut[r] = ok(r) ? rp : S(0);
+      }
+#pragma unroll
+      for (int j = 0; j < MC; ++j) c[j] = S(0);
+#pragma unroll
+      for (int r = 0; r < R; ++r) axpy_<S, MC, true>(c, K[r], ut[r]);
+      stage_cols(c, sb);
+    };
+    auto fwd_collect = [&](int si, S* sb, S* hu, int t) {
+      S* vec0 = sb + L::O_VEC0;
+      collect_cols(si, sb, [&](int k, S tot) {
+        const S vn = F::div_fast(mass(k), tot);
+        vec0[k] = vn;
+        if (rank == 0) hu[size_t(t) * m + k] = vn;
+      });
+    };
+    // A's totals travel while B computes and vice versa: every collect comes
+    // one compute phase after its push
+    for (int t = 1; t <= T; ++t) {
+      fwd_compute(KA, utA, sbA);
+      if (hasB && t > 1) fwd_collect(1, sbB, huB, t - 1);
+      __syncthreads();   // A's partials and B's v~ are published
+      push_cols(0, sbA);
+      if (hasB) fwd_compute(KB, utB, sbB);
+      fwd_collect(0, sbA, huA, t);
+      __syncthreads();   // B's partials and A's v~ are published
+      if (hasB) push_cols(1, sbB);
+    }
+    if (hasB) fwd_collect(1, sbB, huB, T);
+    __syncthreads();
+    // per-item impact terms, float64, completed across the group
+    auto impact = [&](const S (&K)[R][MC], const S (&ut)[R], int u, const S* sb) {
+      S vv[MC];
+#pragma unroll
+      for (int j = 0; j < MC; ++j) vv[j] = sb[L::O_VEC0 + col(j)];
+      const S* const relu = a.rel + size_t(u) * n + r0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int il = lrow(r);
+        const double rr = ok(r) ? double(relu[il]) : 0.0;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < MC; ++j)
+          if (col(j) < m - 1)
+            acc = fma(rr * a.expo_d[min(col(j), m - 2)], double(mul_(mul_(K[r][j], ut[r]), vv[j])), acc);
+        acc = group_sum<double, CG>(acc);
+        if (g == 0 && ok(r)) a.partial[size_t(u) * n + r0 + il] = acc;
+      }
+    };
+    impact(KA, utA, uA, sbA);
+    if (hasB) impact(KB, utB, uB, sbB);
+    __syncthreads();   // the slots are free for the next two users
   }
   cluster.sync();   // keep every CTA's shared memory alive until remote pushes have landed
 }
