@@ -174,9 +174,6 @@ int64_t nsw_solver_launch_count(nsw_solver* s);
 nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT, int32_t* smem_bytes);
 /* Users handled by the tail launch (the wide, latency-oriented tile). */
 int32_t nsw_solver_tail_users(nsw_solver* s);
-/* Cluster tiles: resident clusters of the paired persistent kernel that runs
- * the steady-state steps (0: the tile has none / tolerance schedule). */
-int32_t nsw_solver_pair_clusters(nsw_solver* s);
 /* Measurement helper: evict the L2 (1 GiB write, then discard of those
  * lines) on `stream` (NULL = the solver's stream). */
 nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream);

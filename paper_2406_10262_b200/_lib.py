@@ -73,7 +73,6 @@ SIGNATURES = {
     "nsw_solver_launch_count": (C.c_int64, [_vp]),
     "nsw_solver_variant": (C.c_int, [_vp, C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32), C.POINTER(_i32)]),
     "nsw_solver_tail_users": (_i32, [_vp]),
-    "nsw_solver_pair_clusters": (_i32, [_vp]),
     "nsw_solver_time_steps": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float), C.POINTER(C.c_float)]),
     "nsw_solver_time_fused": (C.c_int, [_vp, _i32, _i32, C.POINTER(C.c_float)]),
     "nsw_solver_phase_times": (C.c_int, [_vp, C.POINTER(C.c_uint64), _i32]),

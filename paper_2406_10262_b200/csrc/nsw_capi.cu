@@ -149,8 +149,6 @@ struct nsw_solver {
   size_t smem = 0;
   const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
   size_t smem2 = 0;
-  int pair_clusters = 0;          // cluster tiles: resident clusters of the paired persistent kernel (0: off)
-  size_t smem_pair = 0;
   int U1 = 0;                     // users in the main launch (U1 == U: no tail launch)
   int imp_chunks = 1;             // user chunks of the impact reduction
   // device state
@@ -215,7 +213,6 @@ void fill_step_args(nsw_solver* s, StepArgs<S>& a) {
   a.bc = s->bc;
   a.tol_mode = s->tol;
   a.chunk = s->opt.tol_chunk > 0 ? s->opt.tol_chunk : 16;
-  a.pair_mode = s->pair_clusters > 0;
   a.res = s->res;
   const double eps = s->cfg.epsilon;
   a.nie = S(-1.0 / eps);
@@ -317,15 +314,6 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
     lc.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelExC(&lc, s->var->fn, s->dtype == NSW_F64 ? args64 : args32));
     s->launches += 1;
-    if (s->pair_clusters > 0) {
-      // steady-state steps (PHASE_RUNNING) run on the paired persistent
-      // kernel: resident clusters walk the users two at a time; the launch
-      // above returned at once for them, this one does for every other phase
-      lc.gridDim = dim3(unsigned(s->pair_clusters) * s->var->CL);
-      lc.dynamicSmemBytes = s->smem_pair;
-      CUDA_TRY(cudaLaunchKernelExC(&lc, s->var->fn_pair, args32));
-      s->launches += 1;
-    }
     return NSW_OK;
   }
   // The tail users are independent of the main launch's users within a step:
@@ -812,39 +800,6 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
                       cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");
-  }
-  // Cluster tiles with a paired persistent kernel (fixed schedule, float32):
-  // as many clusters as the device keeps resident, each walking its users
-  // -- opt-in (NSW_CL_PAIR=1): bit-identical to the one-user cluster kernel,
-  // 5 % slower on config 4 (profiles/r02/ab_cluster_paired.txt)
-  if (!generic && var->CL > 1 && var->fn_pair && !s->tol && s->dtype == NSW_F32 && std::getenv("NSW_CL_PAIR") &&
-      std::atoi(std::getenv("NSW_CL_PAIR")) != 0) {
-    const size_t sm2 = var->smem_pair(T);
-    bool okp = sm2 <= kMaxSmem;
-    if (okp && var->CL > 8)
-      okp = cudaFuncSetAttribute(var->fn_pair, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
-    okp = okp && cudaFuncSetAttribute(var->fn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm2)) == cudaSuccess;
-    int clusters = 0;
-    if (okp) {
-      cudaLaunchConfig_t lc = {};
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = unsigned(var->CL);
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      lc.gridDim = dim3(unsigned(var->CL) * 64u);
-      lc.blockDim = dim3(unsigned(var->NT));
-      lc.dynamicSmemBytes = sm2;
-      lc.attrs = at;
-      lc.numAttrs = 1;
-      okp = cudaOccupancyMaxActiveClusters(&clusters, var->fn_pair, &lc) == cudaSuccess && clusters > 0;
-    }
-    cudaGetLastError();
-    if (okp) {
-      if (const char* e = std::getenv("NSW_CL_PAIR_CLUSTERS"); e && std::atoi(e) > 0) clusters = std::atoi(e);
-      s->pair_clusters = std::min(clusters, users_local);
-      s->smem_pair = sm2;
-    }
   }
   // Wave split: whole waves of the main tile, then (if what is left is at
   // most one user per SM) a tail launch with the wide tile.
@@ -1416,8 +1371,6 @@ nsw_status nsw_solver_variant(nsw_solver* s, int32_t* M, int32_t* R, int32_t* NT
 }
 
 int32_t nsw_solver_tail_users(nsw_solver* s) { return s ? s->U - s->U1 : -1; }
-
-int32_t nsw_solver_pair_clusters(nsw_solver* s) { return s ? s->pair_clusters : -1; }
 
 static nsw_status ensure_flush_buffer(nsw_solver* s) {
   if (s->flush_buf) return NSW_OK;

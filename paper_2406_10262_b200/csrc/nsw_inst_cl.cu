@@ -1,7 +1,7 @@
 // Cluster-tile instantiations (m up to 52, n up to CL * rows-per-CTA):
 // compiled with -DNSW_F64=0|1.
 #include "nsw_registry.h"
-#include "nsw_step_cluster2.cuh"
+#include "nsw_step_cluster.cuh"
 
 #if NSW_F64
 #define NSW_S double
@@ -47,14 +47,7 @@ NSW_REG_CLT(21, 1, 4, 128, 2, 2)
 #if !NSW_F64
 // 9-CTA clusters of 448 items (n <= 4032, config 4): B200's GPCs hold 15
 // resident 8- or 9-CTA clusters, so 9 x 15 = 135 SMs work instead of 120
-template <int MC, int CG, int R, int NT, int CL>
-size_t cl2_smem_of(int T) {
-  return cl2_smem_bytes<NSW_S, MC, CG, R, NT, CL>(T);
-}
-// with the paired persistent kernel for the steady-state steps
-Registrar regcl_pair_9(Variant{NSW_DT, 13 * 4, 7, 256, (const void*)&step_kernel_cl<NSW_S, 13, 4, 7, 256, 9, 1>,
-                               &cl_smem_of<13, 4, 7, 256, 9>, 9, ClTile<NSW_S, 13, 4, 7, 256, 9>::NR, 1,
-                               (const void*)&step_kernel_cl2<NSW_S, 13, 4, 7, 256, 9>, &cl2_smem_of<13, 4, 7, 256, 9>});
+NSW_REG_CLT(13, 4, 7, 256, 9, 1)
 // (two CTAs per SM on 16-CTA clusters -- (13,4,8,128), (7,8,8,256), (13,4,4,256)
 // -- and a 14-warp (13,4,4,448) 9-CTA tile ran 3-19 % slower than the
 // 1-CTA/SM tiles: profiles/r01/r01d_cluster_tile_variants.txt)

@@ -16,10 +16,6 @@ struct Variant {
   int CL = 1;     // CTAs per user (thread-block cluster) ; 1 = one CTA per user
   int rows = 0;   // items per CTA (R * NT for the 1-D tiles)
   int minb = 1;   // __launch_bounds__ min CTAs per SM (register cap)
-  // cluster tiles: the paired persistent kernel for PHASE_RUNNING of the fixed
-  // schedule (nsw_step_cluster2.cuh), nullptr if the tile has none
-  const void* fn_pair = nullptr;
-  size_t (*smem_pair)(int T) = nullptr;
 };
 
 std::vector<Variant>& variant_registry();

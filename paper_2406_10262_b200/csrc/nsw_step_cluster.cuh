@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(NT, MINB) step_kernel_cl(const StepArgs<S> a) 
   S* rmw = colres + 2 * P;                      // [NW] per-warp row-residual maxima
 
   const int phase = a.state[ST_PHASE];
-  if (phase == PHASE_FINISHED || (phase == PHASE_RUNNING && a.pair_mode)) {
+  if (phase == PHASE_FINISHED) {
     cluster.sync();
     return;
   }

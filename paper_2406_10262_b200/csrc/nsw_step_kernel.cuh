@@ -22,7 +22,6 @@ struct StepArgs {
   int user0;     // first user of this launch (the tail launch uses another tile)
   int tol_mode;  // 0: fixed schedule; 1: reference tolerance mode (chunked forward)
   int chunk;     // tolerance mode: inner iterations per forward launch
-  int pair_mode; // cluster tiles: PHASE_RUNNING belongs to the paired persistent kernel (step_kernel_cl skips it)
   double* res;   // tolerance mode: [U][T+1] L-inf marginal residual after iteration t
   S* C;          // [U][n][m] transport costs (the ascent variable)
   S* am;         // [U][n][m] Adam first moment

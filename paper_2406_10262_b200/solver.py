@@ -247,9 +247,6 @@ class DeviceSolver:
         tail = int(self.lib.nsw_solver_tail_users(self.h))
         if tail > 0:
             out.update(tail_users=tail, tail_R=R.value >> 16, tail_NT=NT.value >> 16)
-        pairs = int(self.lib.nsw_solver_pair_clusters(self.h))
-        if pairs > 0:   # cluster tile: steady-state steps on the paired persistent kernel
-            out.update(pair_clusters=pairs)
         return out
 
     def launch_count(self) -> int:

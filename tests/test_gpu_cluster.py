@@ -165,32 +165,3 @@ def test_cluster_fp64_tolerance_long_budget_vs_oracle():
     assert trd.sinkhorn_iterations == tro.sinkhorn_iterations
     assert np.abs(pol.values - xo).max() <= 1e-9
 
-
-
-@pytest.mark.parametrize("U,n,T,outer", [
-    (40, 4000, 12, 5),   # 15 resident clusters x 2-3 users: every pipeline shape (lone Y, pairs, lone X)
-    (5, 3700, 7, 4),     # one user per cluster, ragged last CTA, odd T
-    (3, 4000, 1, 3),     # T = 1: no in-loop exchange of the reverse sweep
-])
-def test_paired_cluster_kernel_bitwise(U, n, T, outer, monkeypatch):
-    """The paired persistent cluster kernel (nsw_step_cluster2.cuh: user X's
-    forward interleaved with user Y's reverse sweep) against the one-user
-    cluster kernel it replaces for the steady-state steps: same arithmetic in
-    the same order, so every output must be bit-identical."""
-    rng = np.random.default_rng(U + T)
-    m = 51
-    rel = np.clip(rng.uniform(0.0, 1.0, (U, n)), 1e-4, 1.0)
-    expo = 1.0 / np.log2(np.arange(2, m + 1))
-    cfg = SolverConfig(epsilon=0.05, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300)
-    out = {}
-    for pair in ("0", "1"):
-        monkeypatch.setenv("NSW_CL_PAIR", pair)
-        with DeviceSolver(rel, expo, n, m, cfg, F32) as s:
-            v = s.variant()
-            assert v["M"] == 52 and v["R"] == 7 and v.get("pair_clusters", 0) == (min(15, U) if pair == "1" else 0), v
-            s.run(outer + 1)
-            out[pair] = {k: s.get(k) for k in ("xbest", "cost", "adam_m", "adam_v", "lvi")}
-            out[pair]["F"] = s.get("objective")[:outer]
-    for k in out["0"]:
-        assert np.array_equal(out["0"][k], out["1"][k]), (k, np.abs(out["0"][k] - out["1"][k]).max())
-    assert np.isfinite(out["1"]["F"]).all() and len(out["1"]["F"]) == outer
