@@ -125,6 +125,17 @@ def test_cfg1_natural_tile_choice_one_step():
     assert v.get("tail_users") == 112 and (v["tail_R"], v["tail_NT"]) == (2, 256)
 
 
+def test_cfg2_natural_tile_choice_multi_wave_one_step():
+    """Config 2 (the bench workload) on 600 users: the automatic choice is the
+    bench's main tile over four whole waves (592 users, one CTA per SM) plus
+    an 8-user tail on the wide tile -- the launch shape of the full 10 000-user
+    run (67 waves + 84) at a size the oracle finishes in seconds."""
+    rel, expo, cfg = make_instance("cfg2", seed=0, user_slice=(0, 600))
+    v = check_one_step("cfg2-600", rel, expo, cfg.epsilon, 8, step=2)
+    assert (v["M"], v["R"], v["NT"]) == (21, 4, 256)
+    assert v.get("tail_users") == 8 and (v["tail_R"], v["tail_NT"]) == (2, 512)
+
+
 def test_cfg4_cluster_tile_one_step():
     """Config-4 shape (4000 x 51, eps 0.01): the 9-CTA thread-block-cluster tile."""
     rel, expo, cfg = make_instance("cfg4", seed=0, user_slice=(0, 2))
