@@ -5,6 +5,7 @@
 // (fused step -> impact reduction -> [caller's exchange] -> finalize),
 // captures it in a CUDA graph, and copies results back in the reference's
 // layouts.  Mirrors solve_fair_ranking (reference solver.py:138-241).
+#include <nvtx3/nvToolsExt.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -36,6 +37,15 @@ std::vector<Variant>& variant_registry() {
 using namespace nsw;
 
 namespace {
+
+// NVTX ranges (header-only nvtx3: a no-op unless a profiler is attached) mark
+// the phases of the C ABI on the timeline: setup, stepping, result download.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 thread_local std::string g_err;
 
@@ -608,6 +618,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
                              const nsw_solver_config* config, const nsw_device_options* options,
                              nsw_solver** out) {
   if (!out || !relevance_local || !exposure || !options) return fail(NSW_ERR_ARG, "NULL argument");
+  NvtxRange nvtx("nsw_solver_create");
   *out = nullptr;
   nsw_status st = validate_config(config);
   if (st != NSW_OK) return st;
@@ -1017,12 +1028,14 @@ nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
 
 nsw_status nsw_solver_local_step(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  NvtxRange nvtx("nsw_solver_local_step");
   DeviceGuard guard(s->device);
   return launch_step(s, stream ? (cudaStream_t)stream : s->stream);
 }
 
 nsw_status nsw_solver_finalize(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  NvtxRange nvtx("nsw_solver_finalize");
   DeviceGuard guard(s->device);
   return launch_finalize(s, stream ? (cudaStream_t)stream : s->stream);
 }
@@ -1185,6 +1198,7 @@ static nsw_status one_step(nsw_solver* s) {
 
 nsw_status nsw_solver_run(nsw_solver* s, int32_t max_steps, int32_t* done) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  NvtxRange nvtx("nsw_solver_run");
   DeviceGuard guard(s->device);
   if (s->world != 1) return fail(NSW_ERR_ARG, "nsw_solver_run drives a single shard (world == 1)");
   if (done) *done = 0;
@@ -1224,6 +1238,7 @@ nsw_status nsw_solver_stream(nsw_solver* s, void** stream) {
 
 nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
+  NvtxRange nvtx("nsw_solver_result");
   DeviceGuard guard(s->device);
   CUDA_TRY(cudaDeviceSynchronize());
   nsw_status e = read_state(s);
@@ -1567,6 +1582,7 @@ nsw_status nsw_solve_fair_ranking(const double* relevance, const double* exposur
                                   int32_t m, const nsw_solver_config* config,
                                   const nsw_device_options* options, double* policy_out, nsw_trace* trace) {
   if (!relevance || !exposure || !config || !options) return fail(NSW_ERR_ARG, "NULL argument");
+  NvtxRange nvtx("nsw_solve_fair_ranking");
   nsw_solver* s = nullptr;
   nsw_status e = nsw_solver_create(relevance, exposure, U, n, m, nullptr, 1, config, options, &s);
   if (e != NSW_OK) return e;
