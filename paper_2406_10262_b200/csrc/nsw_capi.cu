@@ -297,7 +297,10 @@ nsw_status validate_config(const nsw_solver_config* c) {
 // the occupancy-oriented tile; a tail of at most one user per SM (what is
 // left after whole waves) runs as a second launch with the wide tile, which
 // finishes a lone user several times faster.
-nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
+// allow_side = false keeps the tail launch on `st` itself: the body of the
+// tolerance schedule's while-node is its own capture, and the side stream
+// already belongs to the enclosing one (a stream cannot join two captures).
+nsw_status launch_fused(nsw_solver* s, cudaStream_t st, bool allow_side = true) {
   void* args32[] = {&s->a32};
   void* args64[] = {&s->a64};
   if (s->generic) {
@@ -331,7 +334,7 @@ nsw_status launch_fused(nsw_solver* s, cudaStream_t st) {
   // start on SMs as soon as the main wave frees them (joined before the
   // impact reduction).
   const bool both = s->U1 > 0 && s->U1 < s->U;
-  const bool side = both && s->side != nullptr;
+  const bool side = both && s->side != nullptr && allow_side;
   if (side) {
     CUDA_TRY(cudaEventRecord(s->fork, st));
     CUDA_TRY(cudaStreamWaitEvent(s->side, s->fork, 0));
@@ -1115,7 +1118,7 @@ static nsw_status ensure_tol_graph(nsw_solver* s) {
         tol_chunk_max_kernel<<<1, 256, 0, s->body_stream>>>(s->res, s->U, s->T, chunk, s->state, s->tolbuf);
         tol_decide_kernel<<<1, 32, 0, s->body_stream>>>(s->tolbuf, s->T, chunk, s->cfg.sinkhorn_tol, s->state,
                                                          static_cast<unsigned long long>(h));
-        e = launch_fused(s, s->body_stream);
+        e = launch_fused(s, s->body_stream, /*allow_side=*/false);
         cudaGraph_t bg = nullptr;
         const cudaError_t ce2 = cudaStreamEndCapture(s->body_stream, &bg);
         if (ce == cudaSuccess) ce = ce2;

@@ -1,0 +1,82 @@
+"""Randomised parity sweep on the GPU box (not part of the test suite): random
+(users, items, positions, inner iterations, outer steps, epsilon, warm start)
+instances through the public drop-in call, float64 against the oracle at the
+float64 bar and float32 against it at the few-step fp32 bar, fixed and
+tolerance schedules, on whatever tile / streaming path the library picks.
+usage: python scripts/fuzz_parity.py [cases] [seed] [first]  -> one line per case (from case `first` on),
+exit 1 on a violation."""
+import os
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from oracle import nsw_oracle as orc  # checker only
+from paper_2406_10262_b200 import (DeviceOptions, ExposureModel, ProblemShape, RelevanceMatrix, SolverConfig,
+                                   SolverError, solve_fair_ranking)
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 0)
+first = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+bad = 0
+t_start = time.time()
+for c in range(cases):
+    # shapes across the tile families: M in {4, 8, 11, 16, 21, 32}, cluster (m <= 52), streaming (m > 52)
+    m = int(rng.choice([2, 3, 4, 5, 8, 9, 11, 12, 16, 17, 21, 25, 32, 33, 40, 52, 53, 60]))
+    n = int(m + rng.integers(0, 6)) if rng.random() < 0.2 else int(rng.integers(m, max(m + 1, 700)))
+    if rng.random() < 0.1:
+        n = int(rng.integers(2049, 2600))          # beyond the one-CTA tiles
+    U = int(rng.choice([1, 2, 3, 5, 9, 150, 310])) if n * m < 20000 else int(rng.integers(1, 6))
+    T = int(rng.integers(1, 25))
+    outer = int(rng.integers(1, 7))
+    eps = float(rng.choice([0.03, 0.05, 0.1, 0.2, 0.5]))
+    warm = bool(rng.random() < 0.7)
+    schedule = "tolerance" if rng.random() < 0.3 else "fixed"
+    dtype = "float32" if rng.random() < 0.5 else "float64"
+    rel = np.clip(rng.uniform(0.0, 1.0, (U, n)), 1e-4, 1.0).astype(np.float32).astype(np.float64)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    tol = 1e-2 if schedule == "tolerance" else 1e-6   # loose: most solves converge inside T (else SolverError)
+    p = orc.SolverParams(epsilon=eps, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300,
+                         warm_start=warm, sinkhorn_tol=tol, fixed_schedule=schedule == "fixed")
+    cfg = SolverConfig(epsilon=eps, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300,
+                       warm_start=warm, sinkhorn_tol=tol)
+    if c < first:
+        continue
+    tag = f"case {c:3d} U={U} n={n} m={m} T={T} outer={outer} eps={eps} warm={warm} {schedule} {dtype}"
+    try:
+        xo, tro, _ = orc.solve(rel, expo, p)
+        oerr = None
+    except orc.OracleSolverError as e:   # the reference's SolverError (> 50 % unconverged)
+        oerr = e
+    try:
+        pol, tr = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg,
+                                     DeviceOptions(dtype=dtype, schedule=schedule))
+        derr = None
+    except SolverError as e:
+        derr = e
+    if (oerr is None) != (derr is None):
+        # fp32 residuals near the tolerance may flip the > 50 % vote; float64 must agree
+        print(tag, "SolverError mismatch: oracle", bool(oerr), "device", bool(derr), "VIOLATION" if dtype == "float64" else "(fp32 vote)")
+        bad += dtype == "float64"
+        continue
+    if oerr is not None:
+        print(tag, "both raise SolverError")
+        continue
+    xd = pol.values
+    dx = float(np.abs(xd - xo).max())
+    fo, fd = np.array(tro.objective), np.array(tr.objective)
+    same_len = len(fo) == len(fd)
+    df = float(np.abs(fd / fo - 1).max()) if same_len else float("nan")
+    its_ok = schedule != "tolerance" or dtype != "float64" or list(tr.sinkhorn_iterations) == list(tro.sinkhorn_iterations)
+    # a lone user's objective is decided by denormal plan entries (most items
+    # never reach a real position: Imp ~ 1e-300), in the reference as much as
+    # here: F is only compared with at least two users
+    if dtype == "float64":
+        ok = same_len and dx <= 1e-9 and (U == 1 or df <= 1e-11) and its_ok
+    else:
+        ok = same_len and np.isfinite(xd).all() and dx <= 5e-4 and (U == 1 or df <= 1e-5)
+    print(tag, f"|dX|={dx:.2e} rel dF={df:.2e}", "" if ok else "VIOLATION", flush=True)
+    bad += not ok
+print(f"{cases} cases, {bad} violations, {time.time() - t_start:.0f} s")
+sys.exit(1 if bad else 0)

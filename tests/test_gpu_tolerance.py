@@ -79,3 +79,31 @@ def test_tolerance_mode_fp32_runs():
     assert len(t32) == len(t64)
     assert max(abs(a - b) for a, b in zip(t32.sinkhorn_iterations, t64.sinkhorn_iterations)) <= 2
     assert np.abs(np.array(t32.objective) / np.array(t64.objective) - 1).max() < 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol,chunk", [("float64", 1e-2, 0), ("float64", 1e-6, 4), ("float32", 1e-2, 0)])
+def test_tolerance_schedule_with_a_wave_tail(dtype, tol, chunk):
+    """More users than one wave, so the fused step is a main launch plus a
+    tail launch on the side stream: the tolerance schedule's per-step graph
+    (a while-node whose body re-launches the fused step) must capture both --
+    the side stream cannot join the body's capture, which used to crash the
+    default drop-in call (found by scripts/fuzz_parity.py)."""
+    from oracle import nsw_oracle as orc
+    U, n, m, T, outer, eps = 310, 436, 21, 21, 5, 0.2
+    rng = np.random.default_rng(40)
+    rel = np.clip(rng.uniform(0.0, 1.0, (U, n)), 1e-4, 1.0).astype(np.float32).astype(np.float64)
+    expo = 1.0 / np.log2(np.arange(2, m + 1))
+    p = orc.SolverParams(epsilon=eps, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300,
+                         warm_start=False, sinkhorn_tol=tol, fixed_schedule=False)
+    xo, tro, _ = orc.solve(rel, expo, p)
+    cfg = SolverConfig(epsilon=eps, sinkhorn_max_iters=T, outer_max_iters=outer, grad_threshold=1e-300,
+                       warm_start=False, sinkhorn_tol=tol)
+    opts = DeviceOptions(dtype=dtype, schedule="tolerance", **({"tol_chunk": chunk} if chunk else {}))
+    with DeviceSolver(rel, expo, n, m, cfg, opts) as s:
+        assert s.variant().get("tail_users", 0) > 0, s.variant()
+    pol, tr = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg, opts)
+    dx = np.abs(pol.values - xo).max()
+    df = np.abs(np.array(tr.objective) / np.array(tro.objective) - 1).max()
+    print(f"tolerance + tail {dtype} tol={tol}: |dX|={dx:.3e} rel dF={df:.3e} iterations {tr.sinkhorn_iterations}")
+    assert tr.sinkhorn_iterations == tro.sinkhorn_iterations
+    assert (dx <= 1e-9 and df <= 1e-12) if dtype == "float64" else (dx <= 1e-4 and df <= 1e-5)
