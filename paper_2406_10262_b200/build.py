@@ -30,7 +30,7 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE,
 # (f64?, M) instantiations of the fused step kernel; any m <= 32 pads up.
 INSTANCES = [(f64, M) for f64 in (0, 1) for M in (4, 8, 11, 16, 21, 32)]
 
-HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_registry.h", "nsw_step_generic.cuh",
+HEADERS = ["nsw_device.cuh", "nsw_step_kernel.cuh", "nsw_step_cluster.cuh", "nsw_ops_generic.cuh", "nsw_registry.h", "nsw_step_generic.cuh",
            "nsw_generic.h", "nsw_pool.h"]
 
 

@@ -337,6 +337,12 @@ __global__ void cost_from_policy_op(const S* __restrict__ x, size_t count, S neg
   if (!__all_sync(0xffffffffu, ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
 }
 
+}  // namespace
+}  // namespace nsw
+#include "nsw_ops_generic.cuh"
+namespace nsw {
+namespace {
+
 template <typename S, int M>
 size_t fwd_smem(int n) {
   constexpr int P = Pitch<S, M>::value;
@@ -438,6 +444,91 @@ nsw_status launch_bwd(const S* K, const S* hist, const S* lvi, const S* row, con
   return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
 }
 
+// Streaming drivers (nsw_ops_generic.cuh): same contract as run_solve / launch_bwd, any (n, m).
+template <typename S>
+nsw_status gen_run_solve(const S* K, const S* row, const S* col, const S* lvi, int B, int n, int m, int T, double tol,
+                         S* plan, S* lu, S* lv, S* hist, int32_t* iters_out, int32_t* conv_out, double* resid_out,
+                         cudaStream_t st) {
+  const Marg<S> mg{row, col, n, m};
+  const bool tolm = tol > 0.0;
+  const size_t sm_f = 2 * size_t(m) * sizeof(S), sm_n = 3 * size_t(m) * sizeof(S);
+  if (sm_n > 200 * 1024) return NSW_ERR_UNSUPPORTED;   // m beyond ~8000 (float64): no caller of this path
+  auto f1 = gen_fwd_op<S, Marg<S>>;
+  auto f2 = gen_finish_op<S, Marg<S>>;
+  if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_f)) != cudaSuccess ||
+      cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_n)) != cudaSuccess)
+    return NSW_ERR_CUDA;
+  double* res = nullptr;
+  double* rd = nullptr;
+  nsw_status e = NSW_OK;
+  if (private_malloc((void**)&rd, size_t(B) * sizeof(double), st) != cudaSuccess ||
+      (tolm && private_malloc((void**)&res, size_t(B) * (T + 1) * sizeof(double), st) != cudaSuccess))
+    e = NSW_ERR_CUDA;
+  int ts = T;
+  if (e == NSW_OK) {
+    if (!tolm) {
+      f1<<<B, GOP_NT, sm_f, st>>>(K, lvi, mg, B, n, m, T, 0, T, hist, lu, nullptr);
+    } else {
+      std::vector<double> hres(size_t(B) * (T + 1));
+      for (int t0 = 0; t0 < T; t0 += OP_CHUNK) {
+        const int t1 = std::min(t0 + OP_CHUNK, T);
+        f1<<<B, GOP_NT, sm_f, st>>>(K, lvi, mg, B, n, m, T, t0, t1, hist, lu, res);
+        if (cudaMemcpyAsync(hres.data(), res, hres.size() * sizeof(double), cudaMemcpyDeviceToHost, st) !=
+                cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess) {
+          e = NSW_ERR_CUDA;
+          break;
+        }
+        int found = 0;
+        for (int t = t0 + 1; t <= t1 && !found; ++t) {
+          double mx = 0.0;
+          for (int b = 0; b < B; ++b) mx = std::max(mx, hres[size_t(b) * (T + 1) + t]);
+          if (mx <= tol) found = t;   // residual.max() <= tol (sinkhorn.py:244)
+        }
+        if (found) {
+          ts = found;
+          break;
+        }
+      }
+    }
+  }
+  if (e == NSW_OK) {
+    f2<<<B, GOP_NT, sm_n, st>>>(K, lvi, mg, B, n, m, ts, hist, plan, lu, lv, rd);
+    if (cudaGetLastError() != cudaSuccess) e = NSW_ERR_CUDA;
+  }
+  std::vector<double> hr(B, 0.0);
+  if (e == NSW_OK && (resid_out || conv_out)) {
+    if (cudaMemcpyAsync(hr.data(), rd, B * sizeof(double), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      e = NSW_ERR_CUDA;
+  }
+  if (res) cudaFreeAsync(res, st);
+  if (rd) cudaFreeAsync(rd, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) e = NSW_ERR_CUDA;
+  if (e != NSW_OK) return e;
+  if (iters_out) *iters_out = ts;
+  for (int b = 0; b < B; ++b) {
+    if (resid_out) resid_out[b] = hr[b];
+    if (conv_out) conv_out[b] = hr[b] <= tol;   // residual <= tol (sinkhorn.py:253)
+  }
+  return NSW_OK;
+}
+
+template <typename S>
+nsw_status gen_launch_bwd(const S* K, const S* hist, const S* lvi, const S* row, const S* col, const S* gp, const S* X,
+                          const S* lu, int B, int n, int m, int T, S* gk, cudaStream_t st) {
+  const size_t smem = 4 * size_t(m) * sizeof(S);
+  if (smem > 200 * 1024) return NSW_ERR_UNSUPPORTED;
+  auto fn = gen_bwd_op<S, Marg<S>>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    return NSW_ERR_CUDA;
+  S* scratch = nullptr;
+  if (private_malloc((void**)&scratch, size_t(B) * 2 * n * sizeof(S), st) != cudaSuccess) return NSW_ERR_CUDA;
+  fn<<<B, GOP_NT, smem, st>>>(K, hist, lvi, Marg<S>{row, col, n, m}, gp, X, lu, B, n, m, T, gk, scratch);
+  const cudaError_t ce = cudaGetLastError();
+  cudaFreeAsync(scratch, st);
+  return ce == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
+}
+
 template <typename S>
 nsw_status dispatch_solve(const S* K, const S* row, const S* col, const S* lvi, int B, int n, int m, int T, double tol,
                           S* plan, S* lu, S* lv, S* hist, int32_t* iters, int32_t* conv, double* resid, void* stream) {
@@ -445,15 +536,19 @@ nsw_status dispatch_solve(const S* K, const S* row, const S* col, const S* lvi, 
   if (m < 2 || n < 1) return NSW_ERR_SHAPE;
   if (!row && m > n) return NSW_ERR_SHAPE;   // ranking marginals need m <= n
   cudaStream_t st = (cudaStream_t)stream;
-#define NSW_SOLVE(MM) return run_solve<S, MM>(K, row, col, lvi, B, n, m, T, tol, plan, lu, lv, hist, iters, conv, resid, st)
+  // shared-memory tile if one holds the kernel (m <= 32 and n rows fit), else the streaming operators
+  nsw_status e = NSW_ERR_UNSUPPORTED;
+#define NSW_SOLVE(MM) e = run_solve<S, MM>(K, row, col, lvi, B, n, m, T, tol, plan, lu, lv, hist, iters, conv, resid, st)
   if (m <= 4) NSW_SOLVE(4);
-  if (m <= 8) NSW_SOLVE(8);
-  if (m <= 11) NSW_SOLVE(11);
-  if (m <= 16) NSW_SOLVE(16);
-  if (m <= 21) NSW_SOLVE(21);
-  if (m <= 32) NSW_SOLVE(32);
+  else if (m <= 8) NSW_SOLVE(8);
+  else if (m <= 11) NSW_SOLVE(11);
+  else if (m <= 16) NSW_SOLVE(16);
+  else if (m <= 21) NSW_SOLVE(21);
+  else if (m <= 32) NSW_SOLVE(32);
 #undef NSW_SOLVE
-  return NSW_ERR_UNSUPPORTED;
+  if (e == NSW_ERR_UNSUPPORTED)
+    e = gen_run_solve<S>(K, row, col, lvi, B, n, m, T, tol, plan, lu, lv, hist, iters, conv, resid, st);
+  return e;
 }
 
 template <typename S>
@@ -463,15 +558,17 @@ nsw_status dispatch_bwd(const S* K, const S* hist, const S* lvi, const S* row, c
   if (m < 2 || n < 1) return NSW_ERR_SHAPE;
   if (!row && m > n) return NSW_ERR_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
-#define NSW_BWD(MM) return launch_bwd<S, MM>(K, hist, lvi, row, col, gp, X, lu, B, n, m, T, gk, st)
+  nsw_status e = NSW_ERR_UNSUPPORTED;
+#define NSW_BWD(MM) e = launch_bwd<S, MM>(K, hist, lvi, row, col, gp, X, lu, B, n, m, T, gk, st)
   if (m <= 4) NSW_BWD(4);
-  if (m <= 8) NSW_BWD(8);
-  if (m <= 11) NSW_BWD(11);
-  if (m <= 16) NSW_BWD(16);
-  if (m <= 21) NSW_BWD(21);
-  if (m <= 32) NSW_BWD(32);
+  else if (m <= 8) NSW_BWD(8);
+  else if (m <= 11) NSW_BWD(11);
+  else if (m <= 16) NSW_BWD(16);
+  else if (m <= 21) NSW_BWD(21);
+  else if (m <= 32) NSW_BWD(32);
 #undef NSW_BWD
-  return NSW_ERR_UNSUPPORTED;
+  if (e == NSW_ERR_UNSUPPORTED) e = gen_launch_bwd<S>(K, hist, lvi, row, col, gp, X, lu, B, n, m, T, gk, st);
+  return e;
 }
 
 template <typename S>
