@@ -4,7 +4,8 @@ state read back, a fresh solver resumed from it -- against the uninterrupted
 solve; (2) the sharded ascent with 2-4 logical ranks on one GPU (one gathered
 impact buffer, as tests/test_gpu_two_shards.py) against the unsharded solve;
 (3) invalid inputs through the public call: the reference's exception classes,
-never a crash.
+never a crash; (4) the tolerance schedule across 2-3 logical ranks (chunk residual
+maxima combined by MAX before every decide) against the unsharded solve.
 usage: python scripts/fuzz_api.py [cases] [seed] -> one line per case, exit 1 on a violation."""
 import os
 import sys
@@ -41,7 +42,7 @@ def instance():
 
 
 for c in range(cases):
-    kind = c % 3
+    kind = c % 4
     U, n, m, rel, expo, cfg, dtype = instance()
     opts = DeviceOptions(dtype=dtype, schedule="fixed")
     outer = cfg.outer_max_iters
@@ -106,6 +107,76 @@ for c in range(cases):
         df = float(np.abs(np.array(out[0][1].objective) / np.array(t1.objective) - 1).max())
         ok = same and len(out[0][1]) == len(t1) and (dx <= 1e-9 and df <= 1e-12 if dtype == "float64" else dx <= 5e-2 and df <= 1e-5)
         print(tag, f"world={world}: ranks agree {same} |dX|={dx:.1e} rel dF={df:.1e}", "" if ok else "VIOLATION", flush=True)
+    elif kind == 3:
+        # ---- tolerance schedule across logical ranks (float64; SolverError on both sides or neither) ----
+        from paper_2406_10262_b200 import SolverError
+        world = min(int(rng.integers(2, 4)), U)
+        chunk = int(rng.choice([1, 4, 16]))
+        cfg = SolverConfig(epsilon=cfg.epsilon, sinkhorn_max_iters=int(rng.integers(4, 40)), outer_max_iters=outer,
+                           grad_threshold=1e-300, warm_start=cfg.warm_start, sinkhorn_tol=float(rng.choice([1e-2, 1e-4])))
+        opts = DeviceOptions(dtype="float64", schedule="tolerance", tol_chunk=chunk)
+        tag = tag.replace(dtype, "float64") + f" T={cfg.sinkhorn_max_iters} tol={cfg.sinkhorn_tol} chunk={chunk}"
+        rsq = (rel ** 2).sum(axis=0)
+        gathered = torch.zeros(world * (n + 1), dtype=torch.float64, device="cuda")
+        cmax = [torch.zeros(chunk, dtype=torch.float64, device="cuda") for _ in range(world)]
+        solvers = []
+        for r in range(world):
+            s0, s1 = shard_users(U, world, r)
+            s = DeviceSolver(rel[s0:s1], expo, n, m, cfg, opts, rel_sq_sum=rsq, world=world)
+            s.bind_exchange(gathered[r * (n + 1):(r + 1) * (n + 1)].data_ptr(), gathered.data_ptr())
+            s.set_scalar("users_total", U)
+            s.bind_tol_exchange(cmax[r].data_ptr())
+            solvers.append(s)
+        derr = oerr = None
+        try:
+            for _ in range(outer + 1):
+                for s in solvers:
+                    s.local_step()
+                while True:
+                    for s in solvers:
+                        s.tol_local()
+                    torch.cuda.synchronize()
+                    mx = cmax[0].clone()
+                    for cm in cmax[1:]:
+                        mx = torch.maximum(mx, cm)
+                    for cm in cmax:
+                        cm.copy_(mx)
+                    torch.cuda.synchronize()
+                    phases = [s.tol_decide() for s in solvers]
+                    assert len(set(phases)) == 1, phases
+                    if phases[0] in (5, 6):
+                        for s in solvers:
+                            s.local_step()
+                    if phases[0] != 5:
+                        break
+                torch.cuda.synchronize()
+                for s in solvers:
+                    s.finalize()
+                torch.cuda.synchronize()
+                if all(s.status()[0] == 3 for s in solvers):
+                    break
+            try:
+                out = [s.result() for s in solvers]
+            except SolverError as e:
+                derr = e
+        finally:
+            for s in solvers:
+                s.close()
+        try:
+            p1, t1 = solve_fair_ranking(RelevanceMatrix(rel), ExposureModel(expo), ProblemShape(U, n, m), cfg, opts)
+        except SolverError as e:
+            oerr = e
+        if derr is not None or oerr is not None:
+            ok = (derr is None) == (oerr is None)
+            print(tag, f"world={world}: SolverError sharded {derr is not None} unsharded {oerr is not None}",
+                  "" if ok else "VIOLATION", flush=True)
+        else:
+            pol = np.concatenate([p for p, _ in out], axis=0)
+            same = all(t.objective == out[0][1].objective and t.sinkhorn_iterations == t1.sinkhorn_iterations for _, t in out)
+            dx = float(np.abs(pol - p1.values).max())
+            ok = same and dx <= 1e-9
+            print(tag, f"world={world}: traces and iteration counts agree {same} |dX|={dx:.1e} iterations {t1.sinkhorn_iterations}",
+                  "" if ok else "VIOLATION", flush=True)
     else:
         # ---- invalid inputs: the reference's exception classes ----
         which = int(rng.integers(0, 7))
