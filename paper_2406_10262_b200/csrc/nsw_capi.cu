@@ -1351,6 +1351,13 @@ nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value
   else if (!strcmp(field, "step")) idx = ST_STEP;
   else if (!strcmp(field, "improved")) idx = ST_IMPROVED;
   if (idx >= 0) {
+    // the step indexes the per-step trace arrays and the Adam bias-correction
+    // table on the device: an out-of-range value would write past them
+    if (idx == ST_STEP && (value < 0 || value >= s->outer_max))
+      return fail(NSW_ERR_DOMAIN, "step must lie in [0, outer_max_iters)");
+    if (idx == ST_PHASE && (value < PHASE_INIT || value > PHASE_FWD_FIN))
+      return fail(NSW_ERR_DOMAIN, "unknown phase");
+    if (idx == ST_IMPROVED && value != 0 && value != 1) return fail(NSW_ERR_DOMAIN, "improved is 0 or 1");
     int v = int(value);
     CUDA_TRY(cudaMemcpy(s->state + idx, &v, 4, cudaMemcpyHostToDevice));
     return NSW_OK;

@@ -95,3 +95,25 @@ def test_ascent_building_blocks_match_oracle(golden):
                                      cfg.adam_eps)
     assert st2.step == s2 == 2
     assert np.array_equal(p2, q2) and np.array_equal(st2.m, m2) and np.array_equal(st2.v, v2)
+
+
+def test_step_level_state_setters_validate():
+    """nsw_solver_set_scalar: the step indexes the device's per-step trace and
+    bias-correction arrays, so an out-of-range value is rejected (it used to be
+    written through, and the next finalize wrote past the trace)."""
+    from paper_2406_10262_b200 import DeviceOptions, DeviceSolver
+    rng = np.random.default_rng(0)
+    rel = np.clip(rng.uniform(0, 1, (5, 30)), 1e-4, 1)
+    expo = 1.0 / np.log2(np.arange(2, 7))
+    cfg = SolverConfig(epsilon=0.1, sinkhorn_max_iters=5, outer_max_iters=3, grad_threshold=1e-300)
+    with DeviceSolver(rel, expo, 30, 6, cfg, DeviceOptions(dtype="float64", schedule="fixed")) as s:
+        for name, value in (("step", 3), ("step", -1), ("step", 99), ("phase", 7), ("phase", -1), ("improved", 2)):
+            with pytest.raises(DomainError):
+                s.set_scalar(name, value)
+        with pytest.raises(ValueError):
+            s.set_scalar("nope", 1)
+        s.set_scalar("step", 2)      # in range
+        s.set_scalar("step", 0)
+        s.run(4)
+        pol, tr = s.result()
+        assert len(tr) == 3 and np.isfinite(pol).all()
