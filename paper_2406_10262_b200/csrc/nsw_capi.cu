@@ -628,6 +628,23 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
   if (users_local <= 0 || n <= 0 || m < 2 || m > n)
     return fail(NSW_ERR_SHAPE, "need users > 0 and 2 <= num_positions <= num_items");
   if (world < 1) return fail(NSW_ERR_ARG, "world must be >= 1");
+  // the value checks of the reference's ExposureModel (core.py:113-123), same
+  // order and messages: a C caller gets the DomainError the reference would
+  // have raised (the relevance is checked on the device after its upload)
+  {
+    bool finite = true, rising = false;
+    double lo = INFINITY, hi = -INFINITY;
+    for (int k = 0; k < m - 1; ++k) {
+      const double v = exposure[k];
+      finite = finite && std::isfinite(v);
+      lo = std::min(lo, v);
+      hi = std::max(hi, v);
+      if (k > 0 && v > exposure[k - 1]) rising = true;
+    }
+    if (!finite) return fail(NSW_ERR_DOMAIN, "exposure contains non-finite entries");
+    if (lo <= 0.0 || hi > 1.0) return fail(NSW_ERR_DOMAIN, "exposure entries must lie in (0, 1]");
+    if (rising) return fail(NSW_ERR_DOMAIN, "exposure must be non-increasing in position");
+  }
   if (options->dtype != NSW_F32 && options->dtype != NSW_F64) return fail(NSW_ERR_ARG, "bad dtype");
   if (options->schedule != NSW_SCHEDULE_FIXED && options->schedule != NSW_SCHEDULE_TOLERANCE)
     return fail(NSW_ERR_ARG, "bad schedule");
@@ -911,8 +928,24 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
       rel_sq_kernel<<<(n + 127) / 128, 128, 0, s->stream>>>(r64, users_local, n, s->rel_sq);
       ce = cudaGetLastError();
     }
+    // RelevanceMatrix's value checks (core.py:85-93) on the uploaded float64 copy
+    unsigned* flags = nullptr;
+    unsigned hflags = 0;
+    if (ce == cudaSuccess && pool_malloc((void**)&flags, sizeof(unsigned), s->stream) != NSW_OK) ce = cudaErrorMemoryAllocation;
+    if (ce == cudaSuccess) ce = cudaMemsetAsync(flags, 0, sizeof(unsigned), s->stream);
+    if (ce == cudaSuccess) {
+      rel_check_kernel<<<sm_count() * 4, 256, 0, s->stream>>>(r64, cells_r, flags);
+      ce = cudaGetLastError();
+    }
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(&hflags, flags, sizeof(unsigned), cudaMemcpyDeviceToHost, s->stream);
+    if (flags) pool_free(flags, s->stream);
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s->stream);
     if (s->dtype == NSW_F32) pool_free(r64, s->stream);
+    if (ce == cudaSuccess && hflags != 0) {
+      nsw_solver_destroy(s);
+      return fail(NSW_ERR_DOMAIN, (hflags & 1u) ? "relevance contains non-finite entries"
+                                                : "relevance entries must lie in (0, 1]");
+    }
     if (ce != cudaSuccess) {
       nsw_solver_destroy(s);
       return fail(NSW_ERR_CUDA, std::string("relevance upload: ") + cudaGetErrorString(ce));

@@ -255,6 +255,18 @@ __global__ void narrow_kernel(const double* __restrict__ src, float* __restrict_
     dst[i] = __double2float_rn(src[i]);
 }
 
+// bit 0: a non-finite relevance; bit 1: a value outside (0, 1]  (core.py:90-93)
+__global__ void rel_check_kernel(const double* __restrict__ rel, size_t count, unsigned* __restrict__ flags) {
+  unsigned f = 0;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < count; i += size_t(gridDim.x) * blockDim.x) {
+    const double v = rel[i];
+    if (!isfinite(v)) f |= 1u;
+    else if (v <= 0.0 || v > 1.0) f |= 2u;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (f != 0 && (threadIdx.x & 31) == 0) atomicOr(flags, f);
+}
+
 // rsq_i = sum_u r_ui^2 in user order with separate multiply / add roundings
 // (the closed-form gradient norm's item weights, solver.py:211)
 __global__ void rel_sq_kernel(const double* __restrict__ rel, int U, int n, double* __restrict__ rsq) {

@@ -1418,6 +1418,7 @@ __global__ void flush_kernel(float* buf, size_t n);
 __global__ void discard_kernel(float* buf, size_t n);
 __global__ void widen_kernel(const float* __restrict__ src, double* __restrict__ dst, size_t n, unsigned* bad);
 __global__ void narrow_kernel(const double* __restrict__ src, float* __restrict__ dst, size_t n);
+__global__ void rel_check_kernel(const double* __restrict__ rel, size_t count, unsigned* __restrict__ flags);
 __global__ void rel_sq_kernel(const double* __restrict__ rel, int U, int n, double* __restrict__ rsq);
 
 }  // namespace nsw

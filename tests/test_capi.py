@@ -83,6 +83,35 @@ def test_create_rejects_bad_shapes_and_config():
         check(_create(rel, expo, 5, 3, bad, opt))
 
 
+@pytest.mark.parametrize("what,message", [
+    pytest.param("rel_nan", "relevance contains non-finite", marks=pytest.mark.gpu),
+    pytest.param("rel_zero", "relevance entries must lie in (0, 1]", marks=pytest.mark.gpu),
+    pytest.param("rel_big", "relevance entries must lie in (0, 1]", marks=pytest.mark.gpu),
+    ("expo_inf", "exposure contains non-finite"),
+    ("expo_neg", "exposure entries must lie in (0, 1]"), ("expo_rising", "exposure must be non-increasing"),
+])
+def test_create_checks_values_like_the_reference_types(what, message):
+    """A C caller bypasses RelevanceMatrix / ExposureModel: the C ABI applies
+    their value checks itself (core.py:85-93, :113-123) -- the exposure on the
+    host before any device work, the relevance on the device after its upload."""
+    rel = np.full((2, 5), 0.5)
+    expo = np.array([1.0, 0.6])
+    if what == "rel_nan":
+        rel[1, 2] = np.nan
+    elif what == "rel_zero":
+        rel[0, 0] = 0.0
+    elif what == "rel_big":
+        rel[1, 4] = 1.5
+    elif what == "expo_inf":
+        expo[0] = np.inf
+    elif what == "expo_neg":
+        expo[1] = -0.1
+    else:
+        expo = np.array([0.5, 0.6])
+    with pytest.raises(DomainError, match=message.replace("(", "\\(").replace("]", "\\]")):
+        check(_create(rel, expo, 5, 3, _config_c(SolverConfig()), DeviceOptions().to_c()))
+
+
 def test_python_entry_validates_like_reference():
     from paper_2406_10262_b200 import ExposureModel, ProblemShape, RelevanceMatrix, solve_fair_ranking
     rel = RelevanceMatrix(np.full((3, 4), 0.5))
