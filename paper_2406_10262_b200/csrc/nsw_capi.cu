@@ -159,6 +159,7 @@ struct nsw_solver {
   size_t smem = 0;
   const Variant* var2 = nullptr;  // wide, latency-oriented tile of the tail launch
   size_t smem2 = 0;
+  cudaStream_t ext = nullptr;     // last caller-provided stream that carried this solver's work (sharded drivers)
   int U1 = 0;                     // users in the main launch (U1 == U: no tail launch)
   int imp_chunks = 1;             // user chunks of the impact reduction
   // device state
@@ -291,6 +292,23 @@ nsw_status validate_config(const nsw_solver_config* c) {
   if (c->sinkhorn_max_iters <= 0 || c->outer_max_iters <= 0)
     return fail(NSW_ERR_DOMAIN, "iteration budgets must be positive");
   return NSW_OK;
+}
+
+// Work of a solver runs on its own stream (+ the side stream of the tail
+// launch) or on a stream the caller passed to the step-level entry points.
+// Waiting for it never uses cudaDeviceSynchronize: a device-wide wait from one
+// host thread invalidates a CUDA-graph capture another thread has open (every
+// solver captures its step), so concurrent solvers in one process would break.
+cudaStream_t pick_stream(nsw_solver* s, void* stream) {
+  if (!stream) return s->stream;
+  s->ext = (cudaStream_t)stream;
+  return s->ext;
+}
+cudaError_t sync_solver(nsw_solver* s) {
+  cudaError_t ce = cudaStreamSynchronize(s->stream);
+  if (ce == cudaSuccess && s->side) ce = cudaStreamSynchronize(s->side);
+  if (ce == cudaSuccess && s->ext && s->ext != s->stream) ce = cudaStreamSynchronize(s->ext);
+  return ce;
 }
 
 // The fused step over all users: the main launch covers users [0, U1) with
@@ -695,7 +713,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
       if (v.dtype != var->dtype || v.M != var->M || v.CL < 2 || v.CL * v.rows < n || v.smem(T) > kMaxSmem) continue;
       if (v.CL > 8 && cudaFuncSetAttribute(v.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
         continue;
-      if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v.smem(T))) != cudaSuccess)
+      if (allow_smem((const void*)v.fn, size_t(v.smem(T))) != cudaSuccess)
         continue;
       cudaLaunchConfig_t lc = {};
       cudaLaunchAttribute at[1];
@@ -827,7 +845,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
     nsw_solver_destroy(s);
     return fail(NSW_ERR_UNSUPPORTED, "16-CTA clusters are not available on this device");
   }
-  if (!generic && cudaFuncSetAttribute(var->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem)) !=
+  if (!generic && allow_smem((const void*)var->fn, size_t(s->smem)) !=
                       cudaSuccess) {
     nsw_solver_destroy(s);
     return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem) failed");
@@ -850,7 +868,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
             v.smem(T) > kMaxSmem || v.R >= var->R)
           continue;
         int ps = 0;
-        if (cudaFuncSetAttribute(v.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(v.smem(T))) != cudaSuccess ||
+        if (allow_smem((const void*)v.fn, size_t(v.smem(T))) != cudaSuccess ||
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, v.fn, v.NT, v.smem(T)) != cudaSuccess)
           continue;
         if (ps * sms >= users_local &&
@@ -900,7 +918,7 @@ nsw_status nsw_solver_create(const double* relevance_local, const double* exposu
           return fail(NSW_ERR_CUDA, "side stream creation failed");
         }
       }
-      if (cudaFuncSetAttribute(wide->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(s->smem2)) !=
+      if (allow_smem((const void*)wide->fn, size_t(s->smem2)) !=
           cudaSuccess) {
         nsw_solver_destroy(s);
         return fail(NSW_ERR_CUDA, "cudaFuncSetAttribute(smem, tail) failed");
@@ -1049,7 +1067,7 @@ nsw_status nsw_solver_tol_local(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
   DeviceGuard guard(s->device);
   if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
-  return tol_local(s, stream ? (cudaStream_t)stream : s->stream);
+  return tol_local(s, pick_stream(s, stream));
 }
 
 nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
@@ -1057,7 +1075,7 @@ nsw_status nsw_solver_tol_decide(nsw_solver* s, void* stream, int32_t* phase) {
   DeviceGuard guard(s->device);
   if (!s->tol) return fail(NSW_ERR_STATE, "solver is not in the tolerance schedule");
   int ph = 0;
-  nsw_status e = tol_decide(s, stream ? (cudaStream_t)stream : s->stream, &ph);
+  nsw_status e = tol_decide(s, pick_stream(s, stream), &ph);
   if (phase) *phase = ph;
   return e;
 }
@@ -1066,14 +1084,14 @@ nsw_status nsw_solver_local_step(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
   NvtxRange nvtx("nsw_solver_local_step");
   DeviceGuard guard(s->device);
-  return launch_step(s, stream ? (cudaStream_t)stream : s->stream);
+  return launch_step(s, pick_stream(s, stream));
 }
 
 nsw_status nsw_solver_finalize(nsw_solver* s, void* stream) {
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
   NvtxRange nvtx("nsw_solver_finalize");
   DeviceGuard guard(s->device);
-  return launch_finalize(s, stream ? (cudaStream_t)stream : s->stream);
+  return launch_finalize(s, pick_stream(s, stream));
 }
 
 static nsw_status ensure_graph(nsw_solver* s) {
@@ -1276,7 +1294,7 @@ nsw_status nsw_solver_result(nsw_solver* s, double* policy_out, nsw_trace* trace
   if (!s) return fail(NSW_ERR_ARG, "NULL solver");
   NvtxRange nvtx("nsw_solver_result");
   DeviceGuard guard(s->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(sync_solver(s));
   nsw_status e = read_state(s);
   if (e != NSW_OK) return e;
   const int steps = s->state_host[ST_STEP];
@@ -1349,8 +1367,7 @@ nsw_status nsw_solver_get(nsw_solver* s, const char* field, double* host, size_t
   nsw_status e = field_ptr(s, field, &p, &c, &typed);
   if (e != NSW_OK) return e;
   if (count != c) return fail(NSW_ERR_SHAPE, std::string("field ") + field + " has " + std::to_string(c) + " elements");
-  CUDA_TRY(cudaStreamSynchronize(s->stream));
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(sync_solver(s));
   if (!typed) {
     CUDA_TRY(cudaMemcpy(host, p, c * 8, cudaMemcpyDeviceToHost));
     return NSW_OK;
@@ -1367,7 +1384,7 @@ nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, 
   nsw_status e = field_ptr(s, field, &p, &c, &typed);
   if (e != NSW_OK) return e;
   if (count != c) return fail(NSW_ERR_SHAPE, std::string("field ") + field + " has " + std::to_string(c) + " elements");
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(sync_solver(s));
   if (!typed) {
     CUDA_TRY(cudaMemcpy(p, host, c * 8, cudaMemcpyHostToDevice));
     return NSW_OK;
@@ -1378,7 +1395,7 @@ nsw_status nsw_solver_set(nsw_solver* s, const char* field, const double* host, 
 nsw_status nsw_solver_set_scalar(nsw_solver* s, const char* field, int64_t value) {
   if (!s || !field) return fail(NSW_ERR_ARG, "NULL argument");
   DeviceGuard guard(s->device);
-  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(sync_solver(s));
   int idx = -1;
   if (!strcmp(field, "phase")) idx = ST_PHASE;
   else if (!strcmp(field, "step")) idx = ST_STEP;
@@ -1454,7 +1471,7 @@ nsw_status nsw_solver_flush_l2(nsw_solver* s, void* stream) {
   DeviceGuard guard(s->device);
   nsw_status e = ensure_flush_buffer(s);
   if (e != NSW_OK) return e;
-  return launch_l2_flush(s, stream ? (cudaStream_t)stream : s->stream);
+  return launch_l2_flush(s, pick_stream(s, stream));
 }
 
 nsw_status nsw_solver_time_steps(nsw_solver* s, int32_t steps, int32_t flush_l2, float* ms_total,

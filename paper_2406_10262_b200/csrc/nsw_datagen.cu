@@ -246,10 +246,10 @@ nsw_status nsw_datagen_latent(int64_t user0, int32_t users, int32_t n, int32_t d
   const dim3 grid((n + 31) / 32, (users + 31) / 32);
   const size_t smem = size_t(64) * (d + 1) * sizeof(double);
   if (dtype == NSW_F32) {
-    cudaFuncSetAttribute(latent_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    allow_smem((const void*)latent_kernel<float>, size_t(smem));
     latent_kernel<float><<<grid, 256, smem, st>>>(P, Q, b, users, n, d, 1e-6, static_cast<float*>(out));
   } else {
-    cudaFuncSetAttribute(latent_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    allow_smem((const void*)latent_kernel<double>, size_t(smem));
     latent_kernel<double><<<grid, 256, smem, st>>>(P, Q, b, users, n, d, 1e-6, static_cast<double*>(out));
   }
   const cudaError_t e = cudaGetLastError();
@@ -268,11 +268,11 @@ nsw_status nsw_datagen_sparse(int64_t user0, int32_t users, int32_t n, int32_t p
   zipf_logp_kernel<<<(n + 127) / 128, 128, 0, st>>>(logp, n, zipf_s, seed);
   const size_t smem = size_t(n) * sizeof(double);
   if (dtype == NSW_F32) {
-    cudaFuncSetAttribute(sparse_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    allow_smem((const void*)sparse_kernel<float>, size_t(smem));
     sparse_kernel<float><<<users, 256, smem, st>>>(logp, int(user0), n, per_user, floor_value, seed,
                                                    static_cast<float*>(out));
   } else {
-    cudaFuncSetAttribute(sparse_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    allow_smem((const void*)sparse_kernel<double>, size_t(smem));
     sparse_kernel<double><<<users, 256, smem, st>>>(logp, int(user0), n, per_user, floor_value, seed,
                                                     static_cast<double*>(out));
   }

@@ -369,8 +369,8 @@ nsw_status run_solve(const S* K, const S* row, const S* col, const S* lvi, int B
   if (std::max(sf, sn) > 227 * 1024) return NSW_ERR_UNSUPPORTED;
   auto f1 = fwd_chunk_op<S, M>;
   auto f2 = finish_op<S, M>;
-  if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sf)) != cudaSuccess ||
-      cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sn)) != cudaSuccess)
+  if (allow_smem((const void*)f1, size_t(sf)) != cudaSuccess ||
+      allow_smem((const void*)f2, size_t(sn)) != cudaSuccess)
     return NSW_ERR_CUDA;
   const Marg<S> mg{row, col, n, m};
   const bool tolm = tol > 0.0;
@@ -438,7 +438,7 @@ nsw_status launch_bwd(const S* K, const S* hist, const S* lvi, const S* row, con
   const size_t smem = bwd_smem<S, M>(n, T);
   if (smem > 227 * 1024) return NSW_ERR_UNSUPPORTED;
   auto fn = sinkhorn_bwd_op<S, M>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+  if (allow_smem((const void*)fn, size_t(smem)) != cudaSuccess)
     return NSW_ERR_CUDA;
   fn<<<B, OP_NT, smem, st>>>(K, hist, lvi, Marg<S>{row, col, n, m}, gp, X, lu, B, n, m, T, gk);
   return cudaGetLastError() == cudaSuccess ? NSW_OK : NSW_ERR_CUDA;
@@ -455,8 +455,8 @@ nsw_status gen_run_solve(const S* K, const S* row, const S* col, const S* lvi, i
   if (sm_n > 200 * 1024) return NSW_ERR_UNSUPPORTED;   // m beyond ~8000 (float64): no caller of this path
   auto f1 = gen_fwd_op<S, Marg<S>>;
   auto f2 = gen_finish_op<S, Marg<S>>;
-  if (cudaFuncSetAttribute(f1, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_f)) != cudaSuccess ||
-      cudaFuncSetAttribute(f2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_n)) != cudaSuccess)
+  if (allow_smem((const void*)f1, size_t(sm_f)) != cudaSuccess ||
+      allow_smem((const void*)f2, size_t(sm_n)) != cudaSuccess)
     return NSW_ERR_CUDA;
   double* res = nullptr;
   double* rd = nullptr;
@@ -519,7 +519,7 @@ nsw_status gen_launch_bwd(const S* K, const S* hist, const S* lvi, const S* row,
   const size_t smem = 4 * size_t(m) * sizeof(S);
   if (smem > 200 * 1024) return NSW_ERR_UNSUPPORTED;
   auto fn = gen_bwd_op<S, Marg<S>>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+  if (allow_smem((const void*)fn, size_t(smem)) != cudaSuccess)
     return NSW_ERR_CUDA;
   S* scratch = nullptr;
   if (private_malloc((void**)&scratch, size_t(B) * 2 * n * sizeof(S), st) != cudaSuccess) return NSW_ERR_CUDA;

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <utility>
 
 namespace nsw {
 
@@ -15,6 +17,25 @@ struct PoolTable {
   std::mutex mu;
   cudaMemPool_t pool[64] = {};
 };
+
+// Raises a kernel's dynamic shared-memory cap (per device), never lowers it:
+// solvers of different shapes in one process -- in different host threads --
+// share the kernels, and a cap lowered by one between another's setup and its
+// launch would fail that launch.  The cap is a permission, not a request: a
+// launch's carve-out follows the bytes it asks for.
+inline cudaError_t allow_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cap;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& cur = cap[{dev, fn}];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
 
 inline PoolTable& pool_table() {
   static PoolTable t;

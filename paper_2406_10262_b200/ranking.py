@@ -48,5 +48,5 @@ def top_positions(policy):
     fn = lib.nsw_top_positions_f64 if x.dtype == torch.float64 else lib.nsw_top_positions_f32
     stream = torch.cuda.current_stream(x.device).cuda_stream
     check(fn(x.data_ptr(), U, n, m, out.data_ptr(), stream), "top_positions")
-    torch.cuda.synchronize(x.device)
+    torch.cuda.current_stream(x.device).synchronize()   # this call's stream only (a device-wide wait would break another thread's graph capture)
     return out if as_torch else out.cpu().numpy()

@@ -69,7 +69,7 @@ def sinkhorn_batch(log_kernel, log_v_init, iters: int):
     stream = torch.cuda.current_stream(K.device).cuda_stream
     check(fn(K.data_ptr(), lvi.data_ptr(), B, n, m, int(iters), plan.data_ptr(), lu.data_ptr(), lv.data_ptr(),
              hist.data_ptr(), stream), "sinkhorn_batch")
-    torch.cuda.synchronize(K.device)
+    torch.cuda.current_stream(K.device).synchronize()
     return tuple(_out(t, is_t) for t in (plan, lu, lv, hist))
 
 
@@ -94,7 +94,7 @@ def sinkhorn_backward_batch(log_kernel, log_v_hist, log_v_init, grad_plan, plan,
     stream = torch.cuda.current_stream(K.device).cuda_stream
     check(fn(K.data_ptr(), hist.data_ptr(), lvi.data_ptr(), gp.data_ptr(), X.data_ptr(), lu.data_ptr(), B, n, m, T,
              gk.data_ptr(), stream), "sinkhorn_backward_batch")
-    torch.cuda.synchronize(K.device)
+    torch.cuda.current_stream(K.device).synchronize()
     return _out(gk, is_t)
 
 
@@ -167,7 +167,7 @@ def _backward_general(log_kernel, log_v_hist, log_v_init, grad_plan, plan, log_u
     stream = torch.cuda.current_stream(K.device).cuda_stream
     check(fn(K.data_ptr(), r.data_ptr(), c.data_ptr(), hist.data_ptr(), lvi.data_ptr(), gp.data_ptr(), X.data_ptr(),
              lu.data_ptr(), B, n, m, T, gk.data_ptr(), stream), "sinkhorn_backward_general")
-    torch.cuda.synchronize(K.device)
+    torch.cuda.current_stream(K.device).synchronize()
     return _out(gk, is_t)
 
 

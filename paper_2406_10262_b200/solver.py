@@ -493,7 +493,7 @@ def adam_update(params, grads, state: AdamState, config):
     check(fn(P.data_ptr(), G.data_ptr(), Mm.data_ptr(), Vv.data_ptr(), P.numel(), config.adam_lr, b1, b2,
              config.adam_eps, 1.0 - b1 ** step, 1.0 - b2 ** step, torch.cuda.current_stream(P.device).cuda_stream),
           "adam_update")
-    torch.cuda.synchronize(P.device)
+    torch.cuda.current_stream(P.device).synchronize()
     if as_t:
         return P, AdamState(m=Mm, v=Vv, step=step)
     return P.cpu().numpy(), AdamState(m=Mm.cpu().numpy(), v=Vv.cpu().numpy(), step=step)
